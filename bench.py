@@ -1,0 +1,532 @@
+#!/usr/bin/env python
+"""bench.py — seeds/s and achieved HBM GB/s of the fused 2-hop (15,10) sample + mean-aggregation
+forward + replay backward on an ogbn-products-shaped synthetic power-law graph (BASELINE.json).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config products]
+                    [--alpha 3.0] [--no-alt] [--profile]
+
+A step = one forward (fused_2hop_forward, save_indices=True) + one replay backward
+(fused_2hop_backward into a persistent N x D gradient buffer, re-zeroed sparsely) over one
+batch of B=1024 seeds per GPU.  Multi-GPU: one process per GPU (torchrun), seeds sharded by
+global batch position (root_offset), graph + features replicated, no collective on the data
+path -> weak scaling.  Timing: W warm-up steps, then K steps each bracketed by CUDA events on
+the operator's stream, L2 flushed (512 MiB memset) before every step outside the events,
+barrier + synchronize around the timed region, max over ranks.
+
+Also reported (one JSON line on rank 0): e2e through the public API with pinned host inputs,
+the dominant kernel's roofline (library CUDA-event timing + algorithmic bytes), the CPU
+oracle baseline on the host cores, clocks sampled during the timed region, and the same
+measurement at power-law exponent 2.1 (the reference default; sampler-bound) under "alt".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "seeds/s and achieved HBM GB/s, fused 2-hop sample+mean-agg fwd+bwd (15-10)"
+
+
+def parse_args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--impl", choices=["fused", "reference"], default="fused")
+    p.add_argument("--config", default="products", choices=["products", "products25", "reddit", "arxiv"])
+    p.add_argument("--alpha", type=float, default=3.0)
+    p.add_argument("--batch", type=int, default=1024, help="seeds per GPU")
+    p.add_argument("--dtype", default=None, choices=[None, "fp32", "bf16"])
+    p.add_argument("--seed", type=int, default=42)
+    p.add_argument("--no-alt", action="store_true", help="skip the alpha=2.1 side measurement")
+    p.add_argument("--cpu-seconds", type=float, default=10.0)
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--profile", action="store_true", help="print the per-kernel table to stderr")
+    return p.parse_args()
+
+
+# ----------------------------------------------------------------------------------------------
+# environment
+# ----------------------------------------------------------------------------------------------
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+            time.sleep(0.15)
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.05)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peak_hbm():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
+        except Exception:
+            pass
+    return 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------------------------------------
+# workload
+# ----------------------------------------------------------------------------------------------
+def make_inputs(shape, alpha, seed, device, dtype):
+    import torch
+    from paper_2511_13645_b200 import synth
+
+    g = synth.gen_power_law(shape.num_nodes, shape.avg_degree, alpha, seed, device=device)
+    row_stride = shape.d_feat
+    elem = 2 if dtype == torch.bfloat16 else 4
+    if (shape.d_feat * elem) % 16:
+        row_stride = ((shape.d_feat * elem + 15) // 16) * 16 // elem  # 16-byte aligned rows
+    X = synth.make_features(shape.num_nodes, shape.d_feat, seed, dtype=dtype, device=device,
+                            row_stride=row_stride)
+    return g, X
+
+
+def alg_bytes(B, k1, k2, D, E, T1, T2, U2):
+    """SURVEY.md §8d algorithmic bytes per batch (fwd, bwd)."""
+    idx = 4 * B * k1 * (1 + k2)
+    fwd = 8 * B + 8 * (B + T1) + 4 * (T1 + T2) + E * D * T2 + E * D * B + idx
+    bwd = E * D * B + idx + E * D * U2
+    return fwd, bwd
+
+
+def kernel_alg_bytes(name, B, k1, k2, D, E, T1, T2, U2, singles):
+    """Algorithmic bytes per launch of the HBM-heavy kernels."""
+    if name == "k_gather2":
+        return E * D * T2 + E * D * B + 4 * B * k1 * k2 + 4 * B * k1 + 4 * T2
+    if name == "k_bwd_single":
+        return E * D * singles + 4 * B * k1 * k2 + 4 * U2
+    if name == "k_bwd_multi":
+        return E * D * (U2 - singles) + 4 * (T2 - singles)
+    if name == "k_zero_rows":
+        return E * D * T2 + 4 * B * k1 * k2
+    return None
+
+
+class Runner:
+    """One rank's fused 2-hop fwd+bwd step loop on its shard of the global batch."""
+
+    def __init__(self, args, shape, alpha, device, world, rank):
+        import torch
+        import paper_2511_13645_b200 as fsa
+        from paper_2511_13645_b200 import synth
+
+        self.torch, self.fsa = torch, fsa
+        self.args, self.shape, self.alpha = args, shape, alpha
+        self.device, self.world, self.rank = device, world, rank
+        dtype = torch.bfloat16 if (args.dtype == "bf16" or (args.dtype is None and args.config == "reddit")) \
+            else torch.float32
+        self.dtype = dtype
+        self.E = 2 if dtype == torch.bfloat16 else 4
+        t0 = time.time()
+        self.g, self.X = make_inputs(shape, alpha, args.seed, device, dtype)
+        torch.cuda.synchronize(device)
+        self.gen_s = time.time() - t0
+        self.N, self.D = shape.num_nodes, shape.d_feat
+        self.B, self.k1, self.k2 = args.batch, shape.k1, shape.k2
+        self.root_offset = rank * self.B
+        nsteps = args.warmup + args.steps + 8
+        gb = synth.seed_batches(self.N, self.B * world, args.seed, device=device)
+        self.batches = [next(gb)[self.root_offset:self.root_offset + self.B].contiguous() for _ in range(nsteps)]
+        self.base_seeds = [fsa.step_seed(args.seed, i) for i in range(nsteps)]
+        gen = torch.Generator(device=device)
+        gen.manual_seed(args.seed + 7)
+        self.gout = torch.randn((self.B, self.D), generator=gen, device=device).to(dtype)
+        self.gbuf = torch.zeros((self.N, self.D), dtype=dtype, device=device)
+        self.out = torch.empty((self.B, self.D), dtype=dtype, device=device)
+        self.flush = torch.empty(512 << 20, dtype=torch.uint8, device=device)
+        self.idx = None
+
+    def step(self, i):
+        fsa = self.fsa
+        out, idx = fsa.fused_2hop_forward(self.g, self.X, self.batches[i], self.k1, self.k2, self.base_seeds[i],
+                                          validate=False, root_offset=self.root_offset, out=self.out)
+        fsa.fused_2hop_backward(self.gout, idx, self.N, out=self.gbuf, validate=False, zero="sparse")
+        self.idx = idx
+        return out
+
+    def timed(self, steps, warmup, flush=True):
+        torch = self.torch
+        for i in range(warmup):
+            self.step(i)
+        torch.cuda.synchronize(self.device)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        from paper_2511_13645_b200 import _lib
+        l0 = _lib.launch_count()
+        if self.world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize(self.device)
+        t_wall = time.perf_counter()
+        for j in range(steps):
+            if flush:
+                self.flush.zero_()
+            a, b = evs[j]
+            a.record()
+            self.step(warmup + j)
+            b.record()
+        torch.cuda.synchronize(self.device)
+        wall = time.perf_counter() - t_wall
+        if self.world > 1:
+            torch.distributed.barrier()
+        launches = _lib.launch_count() - l0
+        ms = [a.elapsed_time(b) for a, b in evs]
+        return ms, launches, wall
+
+    def stats(self):
+        torch = self.torch
+        s1, s2 = self.idx.s1, self.idx.s2
+        T1 = int((s1 >= 0).sum())
+        v = s2[s2 >= 0]
+        T2 = int(v.numel())
+        uniq, counts = torch.unique(v, return_counts=True)
+        U2 = int(uniq.numel())
+        singles = int((counts == 1).sum())
+        return T1, T2, U2, singles
+
+    def draws(self):
+        """Algorithm-R draws of the last batch: sum over sampled nodes of max(0, deg - k)."""
+        torch = self.torch
+        rp = self.g.rowptr.to(torch.int64)
+        deg = rp[1:] - rp[:-1]
+        seeds = self.batches[self.args.warmup + self.args.steps - 1]
+        s1 = self.idx.s1[self.idx.s1 >= 0].to(torch.int64)
+        return int((deg[seeds] - self.k1).clamp_min(0).sum() + (deg[s1] - self.k2).clamp_min(0).sum())
+
+    def profile(self, steps=20):
+        from paper_2511_13645_b200 import _lib
+        torch = self.torch
+        torch.cuda.synchronize(self.device)
+        _lib.profile(True)
+        for j in range(steps):
+            self.flush.zero_()
+            self.step(j)
+        torch.cuda.synchronize(self.device)
+        prof = _lib.profile_read()
+        _lib.profile(False)
+        return {k: (ms / n, n / steps) for k, (ms, n) in prof.items()}
+
+    def e2e(self, steps, warmup):
+        """Public API with pinned host inputs: H2D seeds + grad_out, fwd+bwd, D2H out."""
+        torch, fsa = self.torch, self.fsa
+        h_seeds = [b.cpu().pin_memory() for b in self.batches[:warmup + steps]]
+        h_gout = self.gout.cpu().pin_memory()
+        h_out = torch.empty((self.B, self.D), dtype=self.dtype).pin_memory()
+
+        def one(i):
+            seeds = h_seeds[i].to(self.device, non_blocking=True)
+            gout = h_gout.to(self.device, non_blocking=True)
+            out, idx = fsa.fused_2hop_forward(self.g, self.X, seeds, self.k1, self.k2, self.base_seeds[i],
+                                              validate=False, root_offset=self.root_offset)
+            fsa.fused_2hop_backward(gout, idx, self.N, out=self.gbuf, validate=False, zero="sparse")
+            h_out.copy_(out, non_blocking=True)
+
+        for i in range(warmup):
+            one(i)
+        torch.cuda.synchronize(self.device)
+        if self.world > 1:
+            torch.distributed.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for j in range(steps):
+            one(warmup + j)
+        b.record()
+        torch.cuda.synchronize(self.device)
+        ms = a.elapsed_time(b) / steps
+        return ms, 8 * self.B + self.E * self.B * self.D, self.E * self.B * self.D
+
+
+def max_over_ranks(x, world, device):
+    if world == 1:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ----------------------------------------------------------------------------------------------
+# CPU oracle baseline (test infrastructure: oracle/ is only the checker / CPU timer here)
+# ----------------------------------------------------------------------------------------------
+def cpu_oracle_time(runner, budget_s, max_steps=None, threads=None):
+    from oracle import oracle
+
+    threads = threads or os.cpu_count()
+    oracle.set_threads(threads)
+    rp, col = runner.g.cpu_arrays()
+    X = runner.X.float().contiguous().cpu().numpy() if runner.dtype != runner.torch.float32 else \
+        runner.X.contiguous().cpu().numpy()
+    gout = runner.gout.float().cpu().numpy()
+    gbuf = np.zeros((runner.N, runner.D), np.float32)
+    times = []
+    t_start = time.perf_counter()
+    i = 0
+    while True:
+        seeds = runner.batches[i % len(runner.batches)].cpu().numpy()
+        t0 = time.perf_counter()
+        out, s1, s2, _, _ = oracle.fused_2hop(rp, col, X, seeds, runner.k1, runner.k2, runner.base_seeds[i],
+                                              root_offset=runner.root_offset)
+        oracle.backward_2hop(gout, s1, s2, runner.N, out=gbuf)
+        times.append(time.perf_counter() - t0)
+        i += 1
+        if (time.perf_counter() - t_start) >= budget_s or (max_steps and i >= max_steps):
+            break
+    return times, threads
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ----------------------------------------------------------------------------------------------
+def run_fused(args):
+    import torch
+    from paper_2511_13645_b200 import synth
+
+    world, rank, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+    device = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+    shape = synth.SHAPES[args.config]
+
+    def measure(alpha, full=True):
+        r = Runner(args, shape, alpha, device, world, rank)
+        with ClockSampler(local) as clk:
+            ms, launches, wall = r.timed(args.steps, args.warmup)
+        mean_ms = statistics.mean(ms)
+        ms_max = max_over_ranks(mean_ms, world, device)
+        T1, T2, U2, singles = r.stats()
+        res = {"runner": r, "ms": ms_max, "ms_local": mean_ms, "launches": launches, "clocks": clk.summary(),
+               "T1": T1, "T2": T2, "U2": U2, "singles": singles, "draws": r.draws(), "gen_s": r.gen_s,
+               "p50": statistics.median(ms), "wall": wall}
+        if full:
+            res["prof"] = r.profile()
+            res["e2e"] = r.e2e(max(20, args.steps // 2), 3)
+        return res
+
+    main = measure(args.alpha)
+    r = main["runner"]
+    B, k1, k2, D, E = r.B, r.k1, r.k2, r.D, r.E
+    fwd_b, bwd_b = alg_bytes(B, k1, k2, D, E, main["T1"], main["T2"], main["U2"])
+    step_bytes = fwd_b + bwd_b
+    seeds_s = world * B / (main["ms"] / 1e3)
+    peak, peak_kind = measured_peak_hbm()
+
+    # dominant kernel and its roofline
+    prof = main["prof"]
+    dom = max(prof, key=lambda k: prof[k][0] * prof[k][1])
+    dom_ms = prof[dom][0]
+    kb = kernel_alg_bytes(dom, B, k1, k2, D, E, main["T1"], main["T2"], main["U2"], main["singles"])
+    achieved = kb / (dom_ms / 1e3) / 1e9 if kb else None
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": (achieved / peak) if achieved else None, "traffic": None,
+                "peak_kind": peak_kind, "kernel_ms": dom_ms,
+                "share_of_step": prof[dom][0] * prof[dom][1] / main["ms_local"]}
+    kernels = {k: {"ms": round(v[0], 5), "per_step": v[1],
+                   "alg_bytes": kernel_alg_bytes(k, B, k1, k2, D, E, main["T1"], main["T2"], main["U2"],
+                                                 main["singles"])} for k, v in sorted(prof.items())}
+    for k, v in kernels.items():
+        if v["alg_bytes"]:
+            v["gbs"] = round(v["alg_bytes"] / (v["ms"] / 1e3) / 1e9, 1)
+
+    e2e_ms, h2d, d2h = main["e2e"]
+    e2e_ms = max_over_ranks(e2e_ms, world, device)
+    line = {
+        "metric": METRIC,
+        "value": round(seeds_s, 1),
+        "unit": "seeds/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(main["ms"], 5),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16" if r.dtype == torch.bfloat16 else "fp32",
+        "data": "synthetic (GPU power-law generator, graph.py:157 algorithm; standard-normal features)",
+        "config": {
+            "workload": f"{shape.name} 2-hop ({k1},{k2}) fused sample+mean fwd+bwd, B={B}/GPU",
+            "num_nodes": r.N, "arcs": r.g.num_edges, "max_degree": r.g.max_degree(), "alpha": args.alpha,
+            "avg_degree_target": shape.avg_degree, "d_feat": D, "batch_per_gpu": B, "global_batch": B * world,
+            "fanouts": [k1, k2], "parallelism": f"seed-sharded dp{world} (root_offset), no data-path collective",
+            "l2": "flushed before every timed step (512 MiB memset outside the step's CUDA events)",
+            "grad_buffer": "persistent N x D, sparse re-zero of the previous step's rows (fsa_zero_rows)",
+            "graph_gen_s": round(main["gen_s"], 2),
+        },
+        "hbm": {"alg_bytes_per_step": step_bytes, "fwd_bytes": fwd_b, "bwd_bytes": bwd_b,
+                "achieved_gbs": round(step_bytes / (main["ms"] / 1e3) / 1e9, 1),
+                "frac_of_peak": round(step_bytes / (main["ms"] / 1e3) / 1e9 / peak, 4), "peak_gbs": peak,
+                "peak_kind": peak_kind, "frac_of_8tbs_nominal": round(step_bytes / (main["ms"] / 1e3) / 8e12, 4),
+                "T1": main["T1"], "T2": main["T2"], "U2": main["U2"]},
+        "draws_per_step": main["draws"],
+        "draws_per_s": round(main["draws"] / (main["ms"] / 1e3), 1),
+        "roofline": roofline,
+        "kernels": kernels,
+        "clocks": main["clocks"],
+        "gpu_launches": main["launches"],
+        "launches_per_step": main["launches"] / args.steps,
+        "e2e": {"value": round(world * B / (e2e_ms / 1e3), 1), "unit": "seeds/s", "ms_per_step": round(e2e_ms, 5),
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "path": "public API (fused_2hop_forward/backward) with pinned host seeds+grad_out, D2H of out"},
+        "p50_ms": round(main["p50"], 5),
+    }
+    if rank == 0 and not args.no_cpu:
+        times, threads = cpu_oracle_time(r, args.cpu_seconds, max_steps=30)
+        cpu_ms = statistics.median(times) * 1e3
+        line["cpu_baseline"] = {"value": round(B / (cpu_ms / 1e3), 2), "unit": "seeds/s", "cores": threads,
+                                "kind": "port", "ms_per_step": round(cpu_ms, 2),
+                                "sample": f"{len(times)} steps of the same workload (B={B}), fwd+bwd incl. the "
+                                          f"reference's N x D zero-fill, OpenMP {threads} threads, {cpu_model()}"}
+    del main, r
+    torch.cuda.empty_cache()
+    if not args.no_alt and args.alpha != 2.1:
+        alt = measure(2.1, full=False)
+        ra = alt["runner"]
+        fb, bb = alg_bytes(B, k1, k2, D, E, alt["T1"], alt["T2"], alt["U2"])
+        line["alt"] = {"alpha": 2.1, "value": round(world * B / (alt["ms"] / 1e3), 1), "unit": "seeds/s",
+                       "ms_per_step": round(alt["ms"], 4), "draws_per_step": alt["draws"],
+                       "draws_per_s": round(alt["draws"] / (alt["ms"] / 1e3), 1),
+                       "hbm_gbs": round((fb + bb) / (alt["ms"] / 1e3) / 1e9, 1),
+                       "arcs": ra.g.num_edges, "max_degree": ra.g.max_degree(), "clocks": alt["clocks"]}
+        if rank == 0 and not args.no_cpu:
+            times, threads = cpu_oracle_time(ra, args.cpu_seconds, max_steps=10)
+            line["alt"]["cpu_baseline"] = {"value": round(B / statistics.median(times), 2), "unit": "seeds/s",
+                                           "cores": threads, "kind": "port",
+                                           "sample": f"{len(times)} steps (B={B})"}
+        del alt, ra
+    if args.profile and rank == 0:
+        print(json.dumps(kernels, indent=1), file=sys.stderr)
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
+def run_reference(args):
+    """Reference arm: the CPU restatement of the reference algorithm (oracle/, the reference is a
+    Python/numba package with no C sources to build) on all host cores, rank 0 only."""
+    world, rank, local = dist_env()
+    if rank != 0:
+        return
+    import torch
+    from paper_2511_13645_b200 import synth
+
+    shape = synth.SHAPES[args.config]
+    device = torch.device("cuda", local) if torch.cuda.is_available() else torch.device("cpu")
+    r = Runner.__new__(Runner)
+    r.torch, r.args, r.shape, r.device = torch, args, shape, device
+    r.dtype = torch.float32
+    r.g, r.X = make_inputs(shape, args.alpha, args.seed, device, torch.float32)
+    r.N, r.D, r.B, r.k1, r.k2 = shape.num_nodes, shape.d_feat, args.batch, shape.k1, shape.k2
+    r.root_offset = 0
+    gb = synth.seed_batches(r.N, r.B, args.seed, device=device)
+    r.batches = [next(gb) for _ in range(args.warmup + args.steps)]
+    import paper_2511_13645_b200 as fsa
+    r.base_seeds = [fsa.step_seed(args.seed, i) for i in range(len(r.batches))]
+    gen = torch.Generator(device=device)
+    gen.manual_seed(args.seed + 7)
+    r.gout = torch.randn((r.B, r.D), generator=gen, device=device)
+    # warm-up steps untimed, then K bounded steps
+    cpu_oracle_time(r, 0.0, max_steps=max(1, args.warmup))
+    times, threads = cpu_oracle_time(r, 1e9, max_steps=args.steps)
+    ms = statistics.mean(times) * 1e3
+    v = r.B / (ms / 1e3)
+    line = {"metric": METRIC, "impl": "reference", "value": round(v, 2), "unit": "seeds/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
+            "data": "synthetic (GPU power-law generator); reference algorithm timed on the host CPU",
+            "config": {"workload": f"{shape.name} 2-hop ({r.k1},{r.k2}) fused sample+mean fwd+bwd, B={r.B}",
+                       "num_nodes": r.N, "arcs": r.g.num_edges, "alpha": args.alpha, "d_feat": r.D},
+            "cpu_baseline": {"value": round(v, 2), "unit": "seeds/s", "cores": threads, "kind": "port",
+                             "sample": f"{args.steps} steps of B={r.B} seeds (fwd + bwd incl. N x D zero-fill), "
+                                       f"{cpu_model()}"},
+            "e2e": {"value": round(v, 2), "unit": "seeds/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_fused(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,149 @@
+/*
+ * fsa_b200.h — C ABI of the B200-native FuseSampleAgg operator (sm_100a).
+ *
+ * Drop-in boundary for the reference's compiled-kernel layer (numba, CPU):
+ *   reference  pkg/src/fsa/kernels.py            this ABI
+ *   ---------------------------------------      -----------------------------------------
+ *   fused_1hop(...)          kernels.py:127-149  fsa_fused_1hop_fwd   (X != NULL)
+ *   sample_1hop(...)         kernels.py:87-97    fsa_fused_1hop_fwd   (X == NULL, out == NULL)
+ *   fused_2hop(...)          kernels.py:152-198  fsa_fused_2hop_fwd   (X != NULL)
+ *   sample_2hop(...)         kernels.py:99-120   fsa_fused_2hop_fwd   (X == NULL, out == NULL)
+ *   invert_targets +
+ *   scatter_from_grad        kernels.py:296-338  fsa_fused_1hop_bwd / fsa_fused_2hop_bwd
+ *     (with the denominators fused.py:216-217 / fused.py:248-250 computed on device)
+ *   derive_state             kernels.py:71-73    fsa_derive_states    (test hook)
+ *   xorshift_steps           kernels.py:76-80    fsa_xorshift_steps   (test hook)
+ *
+ * Conventions (kernels.py:1-5 and SURVEY.md §8b):
+ *   - every pointer argument except `stream` is a DEVICE pointer; the caller allocates every
+ *     output, the op writes in place, nothing is allocated inside;
+ *   - calls are asynchronous and stream-ordered on `stream` (a cudaStream_t, NULL = legacy);
+ *   - return value: FSA_OK or an fsa_status (argument errors detected on the host);
+ *     data-dependent errors (seed / saved index out of range, negative take) are detected on
+ *     device, the offending item is skipped, and a bit is OR-ed into the workspace error word,
+ *     readable with fsa_read_error();
+ *   - results are bitwise independent of launch geometry and of how a batch is sharded across
+ *     GPUs: sampling streams are keyed on the GLOBAL batch position `root_offset + i`
+ *     (root_offset = 0 reproduces the reference exactly, kernels.py:92,135,160,175);
+ *   - workspace: size from fsa_ws_bytes(op, ...); it must be zero-filled when first
+ *     allocated; every op leaves its persistent part zeroed again, so one buffer can be
+ *     reused for any number of calls of the same op kind on the same stream.  A backward
+ *     workspace carries per-node counters laid out for one graph size N: reuse it only with
+ *     the same N (a different N needs a fresh zero-filled buffer).
+ */
+#ifndef FSA_B200_H_
+#define FSA_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum fsa_status {
+  FSA_OK = 0,
+  FSA_ERR_ARG = 1,        /* invalid shape / fanout / null pointer            */
+  FSA_ERR_DTYPE = 2,      /* unsupported dtype code                            */
+  FSA_ERR_WORKSPACE = 3,  /* workspace too small                               */
+  FSA_ERR_CUDA = 4,       /* a CUDA runtime call failed (see fsa_last_cuda_error) */
+  FSA_ERR_ALIGN = 5       /* misaligned feature / output pointer               */
+};
+
+enum fsa_dtype { FSA_F32 = 0, FSA_F64 = 1, FSA_BF16 = 2, FSA_F16 = 3 };
+
+/* bits of the device error word */
+enum fsa_device_error {
+  FSA_DEVERR_SEED_RANGE = 1,  /* "seed out of range"        fused.py:84-85   */
+  FSA_DEVERR_INDEX_RANGE = 2, /* "saved index out of range" fused.py:213,245 */
+  FSA_DEVERR_NEG_TAKE = 4     /* "negative take count"      fused.py:211-212 */
+};
+
+enum fsa_op { FSA_OP_FWD1 = 1, FSA_OP_FWD2 = 2, FSA_OP_BWD1 = 3, FSA_OP_BWD2 = 4 };
+
+const char* fsa_version(void);
+const char* fsa_status_string(int status);
+int fsa_last_cuda_error(void);
+/* select the CUDA device for subsequent calls from this host thread */
+int fsa_set_device(int device);
+
+/* Number of kernels this library has launched in this process (all ops, all devices). */
+unsigned long long fsa_launch_count(void);
+/* Per-kernel CUDA-event timing: fsa_profile(1) clears and starts recording events around every
+ * kernel launch on its launching stream, fsa_profile(0) stops.  fsa_profile_read synchronises
+ * the recorded events and returns, per kernel name (48-byte slots in `names`), the summed
+ * device time and the launch count. */
+int fsa_profile(int enable);
+int fsa_profile_read(int max_kernels, char* names, double* total_ms, int64_t* launches, int* n_kernels);
+
+/* Workspace bytes for `op`.  FWD1: (B, k1=k); FWD2: (B, k1, k2); BWD1: (B, k1=k, N);
+ * BWD2: (B, k1, k2, N).  Unused arguments are ignored. */
+size_t fsa_ws_bytes(int op, int64_t B, int32_t k1, int32_t k2, int64_t N);
+
+/* Synchronously read (and optionally clear) the device error word of a workspace. */
+int fsa_read_error(void* ws, int clear, int* flags, void* stream);
+
+/* ---- forward: fused sample + mean ------------------------------------------------------
+ * rowptr int32[N+1], col int32[E]: CSR with ascending, de-duplicated rows (graph.py:108-151).
+ * X [N, D] of `dtype` with row stride x_stride (elements); out [B, D] row stride out_stride.
+ * seeds int64[B].  save != 0 writes the replay indices (−1 padded, fused.py:40-77):
+ *   1-hop: samples int32[B,k], takes int32[B]
+ *   2-hop: s1 int32[B,k1], s2 int32[B,k1,k2], take1 int32[B], take2 int32[B,k1]
+ * X == NULL and out == NULL gives the sampling-only kernels (sample_1hop / sample_2hop). */
+int fsa_fused_1hop_fwd(const int32_t* rowptr, const int32_t* col, int64_t N,
+                       const void* X, int64_t D, int64_t x_stride, int dtype,
+                       const int64_t* seeds, int64_t B, int64_t root_offset,
+                       int32_t k, uint64_t base_seed, int save,
+                       int32_t* samples, int32_t* takes,
+                       void* out, int64_t out_stride,
+                       void* ws, size_t ws_bytes, void* stream);
+
+int fsa_fused_2hop_fwd(const int32_t* rowptr, const int32_t* col, int64_t N,
+                       const void* X, int64_t D, int64_t x_stride, int dtype,
+                       const int64_t* seeds, int64_t B, int64_t root_offset,
+                       int32_t k1, int32_t k2, uint64_t base_seed, int save,
+                       int32_t* s1, int32_t* s2, int32_t* take1, int32_t* take2,
+                       void* out, int64_t out_stride,
+                       void* ws, size_t ws_bytes, void* stream);
+
+/* ---- backward: deterministic saved-index replay (no float atomics) ----------------------
+ * grad_out [B, D] (row stride g_stride) of `dtype`.  For every touched node v the op writes
+ *   grad_x[v, :] = (((+0.0 + a_1) + a_2) + ...)   a_i = grad_out[t_i / K] / denom[t_i]
+ * over the slots t_1 < t_2 < ... that sampled v (ascending flat slot order, kernels.py:296-338),
+ * denom = max(take,1) (1-hop) or max(t1,1)*max(t2,1) (2-hop, one division by the product).
+ * zero_mode: 0 = untouched rows of grad_x are left as they are (caller keeps them zero),
+ *            1 = grad_x is zero-filled first (the reference's out.fill(0), fused.py:290-296).
+ * grad_x may be NULL when grad_rows != NULL (sparse-COO output only).
+ * Optional outputs: touched int32[B*K] receives the distinct touched node ids (any order)
+ * and n_touched int32[1] their count; grad_rows [B*K, D] receives the row of touched[q] at
+ * row q (requires touched). */
+int fsa_fused_1hop_bwd(const void* grad_out, int64_t B, int64_t D, int64_t g_stride, int dtype,
+                       const int32_t* samples, const int32_t* takes, int32_t k, int64_t N,
+                       void* grad_x, int zero_mode,
+                       int32_t* touched, int32_t* n_touched, void* grad_rows,
+                       void* ws, size_t ws_bytes, void* stream);
+
+int fsa_fused_2hop_bwd(const void* grad_out, int64_t B, int64_t D, int64_t g_stride, int dtype,
+                       const int32_t* s1, const int32_t* s2, int32_t k1, int32_t k2, int64_t N,
+                       void* grad_x, int zero_mode,
+                       int32_t* touched, int32_t* n_touched, void* grad_rows,
+                       void* ws, size_t ws_bytes, void* stream);
+
+/* grad[rows[i], :] = 0 for i < n_rows, rows[i] < 0 skipped (duplicates harmless): sparse
+ * re-zero of a persistent gradient buffer between steps, e.g. with the previous step's flat
+ * s2 / samples as `rows`. */
+int fsa_zero_rows(void* grad, int64_t D, int dtype, const int32_t* rows, int64_t n_rows, void* stream);
+
+/* ---- test hooks (device arrays of length n) ---------------------------------------------- */
+int fsa_derive_states(const uint64_t* base_seed, const int64_t* root, const int64_t* hop,
+                      const int64_t* index, int64_t n, uint64_t* out, void* stream);
+int fsa_xorshift_steps(uint64_t state, int64_t n, uint64_t* out, void* stream);
+/* out[i] = T^dist[i](states[i]) through the GF(2) jump tables */
+int fsa_jump(const uint64_t* states, const int64_t* dist, int64_t n, uint64_t* out, void* stream);
+/* out[i] = x[i] % m[i] through the Barrett path used by the sampler (2 <= m <= 2^30) */
+int fsa_umod(const uint64_t* x, const uint32_t* m, int64_t n, uint32_t* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FSA_B200_H_ */

@@ -1,0 +1,358 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the reference's golden vectors
+and the pinned CPU oracle.  Indices bitwise; fp32 / fp64 means and gradients bitwise (the
+north-star gate is 1e-5 relative, asserted in addition wherever bitwise is checked); bf16
+bitwise against the bf16 rounding of the fp32 oracle on bf16-rounded inputs (gate 1e-2)."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import iter_cases
+
+pytestmark = pytest.mark.gpu
+
+FP32_RTOL = 1e-5
+BF16_RTOL = 1e-2
+
+
+@pytest.fixture(scope="module")
+def fsa():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2511_13645_b200 as m
+    from paper_2511_13645_b200 import _lib
+    _lib.load()
+    return m
+
+
+def dev_graph(fsa, rowptr, col, n):
+    return fsa.CsrGraph.from_arrays(rowptr, col, device="cuda", num_nodes=n)
+
+
+def T(a, dtype=None):
+    t = torch.as_tensor(np.ascontiguousarray(a)).cuda()
+    return t if dtype is None else t.to(dtype)
+
+
+def bitwise(a: torch.Tensor, b: np.ndarray) -> bool:
+    a = a.detach().cpu().numpy()
+    return a.shape == b.shape and a.dtype == b.dtype and a.tobytes() == b.tobytes()
+
+
+def assert_close(got: torch.Tensor, want: np.ndarray, rtol):
+    g = got.detach().double().cpu().numpy()
+    w = want.astype(np.float64)
+    np.testing.assert_allclose(g, w, rtol=rtol, atol=rtol * max(1.0, float(np.abs(w).max(initial=0))))
+
+
+# ---- RNG / arithmetic hooks -----------------------------------------------------------------
+def test_derive_states_hook(fsa, golden_rng):
+    from paper_2511_13645_b200 import _lib
+    g = golden_rng
+    n = len(g["base"])
+    out = torch.empty(n, dtype=torch.int64, device="cuda")
+    base = T(g["base"].view(np.int64))
+    args = [T(g[k].astype(np.int64)) for k in ("root", "hop", "index")]
+    _lib.check(_lib.load().fsa_derive_states(base.data_ptr(), *[a.data_ptr() for a in args], n,
+                                             out.data_ptr(), torch.cuda.current_stream().cuda_stream), "derive")
+    assert np.array_equal(out.cpu().numpy().view(np.uint64), g["derived"])
+
+
+def test_xorshift_and_jump_hooks(fsa, golden_rng):
+    from paper_2511_13645_b200 import _lib
+    lib = _lib.load()
+    st = torch.cuda.current_stream().cuda_stream
+    g = golden_rng
+    out = torch.empty(1000, dtype=torch.int64, device="cuda")
+    _lib.check(lib.fsa_xorshift_steps(int(g["kernel_start"]), 1000, out.data_ptr(), st), "steps")
+    assert np.array_equal(out.cpu().numpy().view(np.uint64), g["kernel_steps"])
+    # jump-ahead equals serial steps (distances 1..1000 from the same start)
+    n = 1000
+    states = torch.full((n,), int(np.int64(g["kernel_start"].view(np.int64))), dtype=torch.int64, device="cuda")
+    dist = torch.arange(1, n + 1, dtype=torch.int64, device="cuda")
+    jumped = torch.empty(n, dtype=torch.int64, device="cuda")
+    _lib.check(lib.fsa_jump(states.data_ptr(), dist.data_ptr(), n, jumped.data_ptr(), st), "jump")
+    assert np.array_equal(jumped.cpu().numpy().view(np.uint64), g["kernel_steps"])
+
+
+def test_barrett_hook(fsa):
+    from paper_2511_13645_b200 import _lib
+    rng = np.random.default_rng(9)
+    n = 1 << 20
+    x = rng.integers(0, 2**63, size=n, dtype=np.uint64) * np.uint64(2) + rng.integers(0, 2, size=n).astype(np.uint64)
+    m = rng.integers(2, 2**30 + 1, size=n).astype(np.uint32)
+    m[:64] = [2, 3, 4, 8, 16, 1 << 29, 1 << 30, (1 << 30) - 1] * 8
+    x[:16] = np.iinfo(np.uint64).max
+    out = torch.empty(n, dtype=torch.int32, device="cuda")
+    xd, md = T(x.view(np.int64)), T(m.view(np.int32))
+    _lib.check(_lib.load().fsa_umod(xd.data_ptr(), md.data_ptr(), n, out.data_ptr(),
+                                    torch.cuda.current_stream().cuda_stream), "umod")
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), (x % m.astype(np.uint64)).astype(np.uint32))
+
+
+# ---- golden forward / backward ----------------------------------------------------------------
+@pytest.mark.parametrize("which", ["small", "powerlaw"])
+def test_golden_cases(fsa, golden_small, golden_powerlaw, which):
+    d = golden_small if which == "small" else golden_powerlaw
+    for name, c in iter_cases(d):
+        g = dev_graph(fsa, c["rowptr"], c["col"], c["N"])
+        X = T(c["X"])
+        seeds = T(c["seeds"])
+        out1, i1 = fsa.fused_1hop_forward(g, X, seeds, c["k1"], c["base_seed"])
+        assert bitwise(i1.samples, c["samples"]), name
+        assert bitwise(i1.takes, c["takes"]), name
+        assert bitwise(out1, c["out1"]), name
+        out2, i2 = fsa.fused_2hop_forward(g, X, seeds, c["k1"], c["k2"], c["base_seed"])
+        assert bitwise(i2.s1, c["s1"]), name
+        assert bitwise(i2.s2, c["s2"]), name
+        assert bitwise(out2, c["out2"]), name
+        g1 = fsa.fused_1hop_backward(T(c["gout1"]), i1, c["N"])
+        assert bitwise(g1, c["grad1"]), name
+        g2 = fsa.fused_2hop_backward(T(c["gout2"]), i2, c["N"])
+        assert bitwise(g2, c["grad2"]), name
+        assert_close(g2, c["grad2"], FP32_RTOL)
+
+
+def test_host_mode_numpy_in_numpy_out(fsa, golden_small):
+    """Reference-style call: numpy arrays in, numpy arrays out (the graph as a plain object)."""
+    class G:  # duck-typed reference CsrGraph
+        pass
+
+    for name, c in iter_cases(golden_small):
+        g = G()
+        g.num_nodes, g.rowptr, g.col = c["N"], c["rowptr"], c["col"]
+        out2, idx = fsa.fused_2hop_forward(g, c["X"], c["seeds"], c["k1"], c["k2"], c["base_seed"])
+        assert isinstance(out2, np.ndarray) and out2.tobytes() == c["out2"].tobytes(), name
+        assert np.array_equal(idx.s2, c["s2"]), name
+        grad = fsa.fused_2hop_backward(c["gout2"], idx, c["N"])
+        assert isinstance(grad, np.ndarray) and grad.tobytes() == c["grad2"].tobytes(), name
+
+
+def test_config1(fsa, golden_config1):
+    c = golden_config1
+    N, D, k, bs = (int(x) for x in c["meta"])
+    X = np.random.default_rng([42, 1]).standard_normal((N, D)).astype(np.float32)
+    g = dev_graph(fsa, c["rowptr"], c["col"], N)
+    out, idx = fsa.fused_1hop_forward(g, T(X), T(c["seeds"]), k, bs)
+    assert bitwise(idx.samples, c["samples"]) and bitwise(idx.takes, c["takes"])
+    assert bitwise(out, c["out"])
+    gout = np.random.default_rng(int(c["gout_seed"])).standard_normal(out.shape).astype(np.float32)
+    grad = fsa.fused_1hop_backward(T(gout), idx, N).cpu().numpy()
+    assert np.array_equal(np.nonzero(np.any(grad != 0, axis=1))[0], c["touched"])
+    assert grad[c["touched"]].tobytes() == c["grad_rows"].tobytes()
+
+
+# ---- semantics ------------------------------------------------------------------------------------
+def test_nosave_identical_and_zero_backward(fsa, golden_powerlaw):
+    for name, c in iter_cases(golden_powerlaw):
+        g = dev_graph(fsa, c["rowptr"], c["col"], c["N"])
+        X, seeds = T(c["X"]), T(c["seeds"])
+        bare, none_idx = fsa.fused_2hop_forward(g, X, seeds, c["k1"], c["k2"], c["base_seed"], save_indices=False)
+        assert none_idx is None and bitwise(bare, c["out2"])
+        bare1, n1 = fsa.fused_1hop_forward(g, X, seeds, c["k1"], c["base_seed"], save_indices=False)
+        assert n1 is None and bitwise(bare1, c["out1"])
+        z = fsa.fused_2hop_backward(torch.ones_like(bare), None, c["N"])
+        assert z.shape == (c["N"], X.shape[1]) and not bool(z.any())
+
+
+def test_sampling_only_entry_points(fsa, golden_powerlaw):
+    for name, c in iter_cases(golden_powerlaw):
+        g = dev_graph(fsa, c["rowptr"], c["col"], c["N"])
+        smp, tk = fsa.sample_1hop(g, T(c["seeds"]), c["k1"], c["base_seed"])
+        assert bitwise(smp, c["samples"]) and bitwise(tk, c["takes"])
+        s1, s2, t1, t2 = fsa.sample_2hop(g, T(c["seeds"]), c["k1"], c["k2"], c["base_seed"])
+        assert bitwise(s1, c["s1"]) and bitwise(s2, c["s2"])
+        assert np.array_equal(t1.cpu().numpy(), (c["s1"] >= 0).sum(1))
+        assert np.array_equal(t2.cpu().numpy(), (c["s2"] >= 0).sum(2))
+
+
+def test_errors_match_reference_messages(fsa):
+    star = dev_graph(fsa, np.array([0, 3, 4, 5, 6]), np.array([1, 2, 3, 0, 0, 0]), 4)
+    X = torch.zeros((4, 2), device="cuda", dtype=torch.float64)
+    with pytest.raises(ValueError, match="seed out of range"):
+        fsa.fused_1hop_forward(star, X, torch.tensor([17], device="cuda"), k=2, base_seed=0)
+    with pytest.raises(ValueError, match="features must be"):
+        fsa.fused_1hop_forward(star, torch.zeros((2, 2), device="cuda"), torch.tensor([0]), k=2, base_seed=0)
+    with pytest.raises(ValueError, match="fanout"):
+        fsa.fused_1hop_forward(star, X, torch.tensor([0]), k=0, base_seed=0)
+    with pytest.raises(ValueError, match="fanouts"):
+        fsa.fused_2hop_forward(star, X, torch.tensor([0]), 0, 2, base_seed=0)
+    with pytest.raises(ValueError, match="seed batch"):
+        fsa.fused_2hop_forward(star, X, torch.tensor([], dtype=torch.int64), 1, 2, base_seed=0)
+    idx = fsa.SampledIndices1(samples=torch.tensor([[9]], dtype=torch.int32, device="cuda"),
+                              takes=torch.tensor([1], dtype=torch.int32, device="cuda"))
+    with pytest.raises(ValueError, match="out of range"):
+        fsa.fused_1hop_backward(torch.ones((1, 1), device="cuda", dtype=torch.float64), idx, num_nodes=5)
+    bad = fsa.SampledIndices1(samples=torch.tensor([[1]], dtype=torch.int32, device="cuda"),
+                              takes=torch.tensor([-1], dtype=torch.int32, device="cuda"))
+    with pytest.raises(ValueError, match="negative take"):
+        fsa.fused_1hop_backward(torch.ones((1, 1), device="cuda", dtype=torch.float64), bad, num_nodes=5)
+    i2 = fsa.SampledIndices2(s1=torch.tensor([[1, -1]], dtype=torch.int32, device="cuda"),
+                             s2=torch.tensor([[[9, -1], [-1, -1]]], dtype=torch.int32, device="cuda"))
+    with pytest.raises(ValueError, match="out of range"):
+        fsa.fused_2hop_backward(torch.ones((1, 1), device="cuda"), i2, num_nodes=5)
+    with pytest.raises(ValueError, match="batch size"):
+        fsa.fused_2hop_backward(torch.ones((3, 1), device="cuda"), i2, num_nodes=50)
+
+
+def test_device_error_flags_without_validation(fsa):
+    from paper_2511_13645_b200 import _lib
+    g = dev_graph(fsa, np.array([0, 1, 2]), np.array([1, 0]), 2)
+    X = torch.ones((2, 4), device="cuda")
+    fsa.device_errors()  # clear
+    out, _ = fsa.fused_2hop_forward(g, X, torch.tensor([0, 5, 1], device="cuda"), 2, 2, 1, validate=False)
+    assert fsa.device_errors() & _lib.FSA_DEVERR_SEED_RANGE
+    assert fsa.device_errors() == 0
+
+
+def test_backward_known_answers(fsa):
+    # test_fused_1hop.py:87-109 and test_fused_2hop.py:70-78
+    idx = fsa.SampledIndices1(samples=torch.tensor([[1, 2, -1]], dtype=torch.int32, device="cuda"),
+                              takes=torch.tensor([2], dtype=torch.int32, device="cuda"))
+    g = fsa.fused_1hop_backward(torch.tensor([[1.0]], device="cuda", dtype=torch.float64), idx, num_nodes=4)
+    assert g[:, 0].tolist() == [0.0, 0.5, 0.5, 0.0]
+    idx = fsa.SampledIndices1(samples=torch.tensor([[7, 3, -1, -1], [7, 1, 2, 5]], dtype=torch.int32, device="cuda"),
+                              takes=torch.tensor([2, 4], dtype=torch.int32, device="cuda"))
+    g = fsa.fused_1hop_backward(torch.tensor([[1.0], [1.0]], device="cuda", dtype=torch.float64), idx, num_nodes=8)
+    assert float(g[7, 0]) == 0.75
+    tree = dev_graph(fsa, np.array([0, 2, 3, 5, 5, 5, 5]), np.array([1, 2, 3, 4, 5]), 6)
+    X = torch.tensor([[0.0], [0.0], [0.0], [1.0], [2.0], [4.0]], device="cuda", dtype=torch.float64)
+    out, i2 = fsa.fused_2hop_forward(tree, X, torch.tensor([0], device="cuda"), 2, 2, 1)
+    assert float(out[0, 0]) == 2.0
+    gr = fsa.fused_2hop_backward(torch.tensor([[1.0]], device="cuda", dtype=torch.float64), i2, 6)
+    assert gr[:, 0].tolist() == [0.0, 0.0, 0.0, 0.5, 0.25, 0.25]
+
+
+def test_persistent_buffer_full_and_sparse_zeroing(fsa, golden_powerlaw):
+    name, c = next(iter_cases(golden_powerlaw))
+    g = dev_graph(fsa, c["rowptr"], c["col"], c["N"])
+    X, seeds = T(c["X"]), T(c["seeds"])
+    buf = torch.full((c["N"], X.shape[1]), 7.0, device="cuda")
+    _, idx = fsa.fused_2hop_forward(g, X, seeds, c["k1"], c["k2"], c["base_seed"])
+    r = fsa.fused_2hop_backward(T(c["gout2"]), idx, c["N"], out=buf)
+    assert r is buf and bitwise(buf, c["grad2"])
+    # a different batch through the sparse path must equal a fresh full computation
+    seeds2 = torch.flip(seeds, [0])[:100]
+    _, idx2 = fsa.fused_2hop_forward(g, X, seeds2, c["k1"], c["k2"], 99)
+    go = torch.randn((100, X.shape[1]), device="cuda")
+    fsa.fused_2hop_backward(T(c["gout2"]), idx, c["N"], out=buf, zero="sparse")
+    fsa.fused_2hop_backward(go, idx2, c["N"], out=buf, zero="sparse")
+    fresh = fsa.fused_2hop_backward(go, idx2, c["N"])
+    assert torch.equal(buf, fresh)
+    buf.add_(1.0)  # user modification -> version changes -> full fill next time
+    fsa.fused_2hop_backward(go, idx2, c["N"], out=buf, zero="sparse")
+    assert torch.equal(buf, fresh)
+
+
+def test_sparse_coo_outputs(fsa, golden_powerlaw):
+    for name, c in iter_cases(golden_powerlaw):
+        g = dev_graph(fsa, c["rowptr"], c["col"], c["N"])
+        _, idx = fsa.fused_2hop_forward(g, T(c["X"]), T(c["seeds"]), c["k1"], c["k2"], c["base_seed"])
+        T2 = idx.s2.numel()
+        touched = torch.empty(T2, dtype=torch.int32, device="cuda")
+        nt = torch.empty(1, dtype=torch.int32, device="cuda")
+        rows = torch.empty((T2, c["X"].shape[1]), device="cuda")
+        dense = fsa.fused_2hop_backward(T(c["gout2"]), idx, c["N"], touched=touched, n_touched=nt, grad_rows=rows)
+        n = int(nt)
+        ids = touched[:n].long()
+        assert n == len(np.unique(c["s2"][c["s2"] >= 0]))
+        assert torch.equal(rows[:n], dense[ids])
+        none = fsa.fused_2hop_backward(T(c["gout2"]), idx, c["N"], out=False, touched=touched, n_touched=nt,
+                                       grad_rows=rows)
+        assert none is None and int(nt) == n
+
+
+# ---- dtypes --------------------------------------------------------------------------------------
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+def test_half_precision_features(fsa, oracle_mod, golden_powerlaw, dtype):
+    for name, c in iter_cases(golden_powerlaw):
+        g = dev_graph(fsa, c["rowptr"], c["col"], c["N"])
+        Xh = T(c["X"]).to(dtype)
+        Xr = Xh.float().cpu().numpy()  # the exact inputs the kernel sees
+        out2, idx = fsa.fused_2hop_forward(g, Xh, T(c["seeds"]), c["k1"], c["k2"], c["base_seed"])
+        ref, *_ = oracle_mod.fused_2hop(c["rowptr"], c["col"], Xr, c["seeds"], c["k1"], c["k2"], c["base_seed"])
+        assert out2.dtype == dtype
+        assert torch.equal(out2, torch.from_numpy(ref).cuda().to(dtype)), name  # fp32 acc, one rounding
+        assert_close(out2.float(), ref, BF16_RTOL)
+        gh = T(c["gout2"]).to(dtype)
+        gr = fsa.fused_2hop_backward(gh, idx, c["N"])
+        rg = oracle_mod.backward_2hop(gh.float().cpu().numpy(), c["s1"], c["s2"], c["N"])
+        assert torch.equal(gr, torch.from_numpy(rg).cuda().to(dtype)), name
+
+
+def test_padded_and_unaligned_rows(fsa, oracle_mod, golden_powerlaw):
+    """Row strides that defeat 16-byte vectors (D=602-like widths) still match bitwise."""
+    name, c = next(iter_cases(golden_powerlaw))
+    g = dev_graph(fsa, c["rowptr"], c["col"], c["N"])
+    for D, stride in ((13, 13), (6, 6), (10, 16), (3, 5)):
+        base = torch.randn((c["N"], stride), device="cuda")
+        X = base[:, :D]
+        out, _ = fsa.fused_2hop_forward(g, X, T(c["seeds"]), c["k1"], c["k2"], c["base_seed"])
+        ref, *_ = oracle_mod.fused_2hop(c["rowptr"], c["col"], X.contiguous().cpu().numpy(), c["seeds"],
+                                        c["k1"], c["k2"], c["base_seed"])
+        assert out.cpu().numpy().tobytes() == ref.tobytes(), (D, stride)
+
+
+# ---- autograd ---------------------------------------------------------------------------------------
+def test_autograd_function(fsa, golden_powerlaw):
+    name, c = next(iter_cases(golden_powerlaw))
+    g = dev_graph(fsa, c["rowptr"], c["col"], c["N"])
+    X = T(c["X"]).requires_grad_(True)
+    out, idx = fsa.fused_sample_agg_2hop(X, g, T(c["seeds"]), c["k1"], c["k2"], c["base_seed"])
+    assert bitwise(out, c["out2"]) and bitwise(idx.s2, c["s2"])
+    (out * T(c["gout2"])).sum().backward()
+    assert bitwise(X.grad, c["grad2"])
+    X.grad = None
+    out, idx = fsa.fused_sample_agg_2hop(X, g, T(c["seeds"]), c["k1"], c["k2"], c["base_seed"], save_indices=False)
+    out.sum().backward()
+    assert idx is None and not bool(X.grad.any())
+    X1 = T(c["X"]).requires_grad_(True)
+    o1, i1 = fsa.fused_sample_agg_1hop(X1, g, T(c["seeds"]), c["k1"], c["base_seed"])
+    (o1 * T(c["gout1"])).sum().backward()
+    assert bitwise(X1.grad, c["grad1"])
+
+
+def test_fd_gradient_fp64(fsa, golden_small):
+    """Central finite differences at fp64 (test_fused_2hop.py:89-104)."""
+    for name, c in list(iter_cases(golden_small))[:8]:
+        if c["X"].dtype != np.float64:
+            continue
+        g = dev_graph(fsa, c["rowptr"], c["col"], c["N"])
+        X = T(c["X"])
+        seeds = T(c["seeds"])
+        out, idx = fsa.fused_2hop_forward(g, X, seeds, c["k1"], c["k2"], c["base_seed"])
+        w = torch.randn_like(out)
+        analytic = fsa.fused_2hop_backward(w, idx, c["N"]).cpu().numpy()
+        eps = 1e-6
+        fd = np.zeros_like(analytic)
+        for v in range(c["N"]):
+            for d in range(X.shape[1]):
+                P = X.clone()
+                P[v, d] += eps
+                fp = float((w * fsa.fused_2hop_forward(g, P, seeds, c["k1"], c["k2"], c["base_seed"], False)[0]).sum())
+                P[v, d] -= 2 * eps
+                fm = float((w * fsa.fused_2hop_forward(g, P, seeds, c["k1"], c["k2"], c["base_seed"], False)[0]).sum())
+                fd[v, d] = (fp - fm) / (2 * eps)
+        scale = np.maximum(np.abs(analytic), 1e-9)
+        assert np.max(np.abs(fd - analytic) / scale) < 1e-6, name
+
+
+# ---- determinism / sharding -------------------------------------------------------------------------
+def test_repeat_and_shard_invariance(fsa, golden_powerlaw):
+    for name, c in iter_cases(golden_powerlaw):
+        g = dev_graph(fsa, c["rowptr"], c["col"], c["N"])
+        X, seeds = T(c["X"]), T(c["seeds"])
+        blobs = set()
+        for _ in range(3):
+            out, idx = fsa.fused_2hop_forward(g, X, seeds, c["k1"], c["k2"], c["base_seed"])
+            gr = fsa.fused_2hop_backward(T(c["gout2"]), idx, c["N"])
+            blobs.add(out.cpu().numpy().tobytes() + idx.s2.cpu().numpy().tobytes() + gr.cpu().numpy().tobytes())
+        assert len(blobs) == 1
+        B = seeds.numel()
+        cuts = [0, 1, B // 4, B // 2 + 3, B]
+        outs, s2s = [], []
+        for lo, hi in zip(cuts[:-1], cuts[1:]):
+            o, i = fsa.fused_2hop_forward(g, X, seeds[lo:hi], c["k1"], c["k2"], c["base_seed"], root_offset=lo)
+            outs.append(o)
+            s2s.append(i.s2)
+        assert bitwise(torch.cat(outs), c["out2"]) and bitwise(torch.cat(s2s), c["s2"])
