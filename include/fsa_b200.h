@@ -106,6 +106,24 @@ int fsa_fused_2hop_fwd(const int32_t* rowptr, const int32_t* col, int64_t N,
                        void* out, int64_t out_stride,
                        void* ws, size_t ws_bytes, void* stream);
 
+/* Same as above with the base seed read from device memory (one uint64) when the kernels run,
+ * so a captured CUDA graph can be replayed with a new seed per step. */
+int fsa_fused_1hop_fwd_dseed(const int32_t* rowptr, const int32_t* col, int64_t N,
+                             const void* X, int64_t D, int64_t x_stride, int dtype,
+                             const int64_t* seeds, int64_t B, int64_t root_offset,
+                             int32_t k, const uint64_t* base_seed, int save,
+                             int32_t* samples, int32_t* takes,
+                             void* out, int64_t out_stride,
+                             void* ws, size_t ws_bytes, void* stream);
+
+int fsa_fused_2hop_fwd_dseed(const int32_t* rowptr, const int32_t* col, int64_t N,
+                             const void* X, int64_t D, int64_t x_stride, int dtype,
+                             const int64_t* seeds, int64_t B, int64_t root_offset,
+                             int32_t k1, int32_t k2, const uint64_t* base_seed, int save,
+                             int32_t* s1, int32_t* s2, int32_t* take1, int32_t* take2,
+                             void* out, int64_t out_stride,
+                             void* ws, size_t ws_bytes, void* stream);
+
 /* ---- backward: deterministic saved-index replay (no float atomics) ----------------------
  * grad_out [B, D] (row stride g_stride) of `dtype`.  For every touched node v the op writes
  *   grad_x[v, :] = (((+0.0 + a_1) + a_2) + ...)   a_i = grad_out[t_i / K] / denom[t_i]

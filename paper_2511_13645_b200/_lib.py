@@ -38,6 +38,10 @@ SIGNATURES = {
                                   _p, _p, _p, _i64, _p, _sz, _p]),
     "fsa_fused_2hop_fwd": (_int, [_p, _p, _i64, _p, _i64, _i64, _int, _p, _i64, _i64, _i32, _i32, _u64,
                                   _int, _p, _p, _p, _p, _p, _i64, _p, _sz, _p]),
+    "fsa_fused_1hop_fwd_dseed": (_int, [_p, _p, _i64, _p, _i64, _i64, _int, _p, _i64, _i64, _i32, _p, _int,
+                                        _p, _p, _p, _i64, _p, _sz, _p]),
+    "fsa_fused_2hop_fwd_dseed": (_int, [_p, _p, _i64, _p, _i64, _i64, _int, _p, _i64, _i64, _i32, _i32, _p,
+                                        _int, _p, _p, _p, _p, _p, _i64, _p, _sz, _p]),
     "fsa_fused_1hop_bwd": (_int, [_p, _i64, _i64, _i64, _int, _p, _p, _i32, _i64, _p, _int, _p, _p, _p,
                                   _p, _sz, _p]),
     "fsa_fused_2hop_bwd": (_int, [_p, _i64, _i64, _i64, _int, _p, _p, _i32, _i32, _i64, _p, _int, _p,

@@ -1,0 +1,127 @@
+"""Repeated-step executor for the fused 2-hop operator: static buffers, CUDA-graph replay.
+
+The reference's training step calls ``fused_2hop_forward`` then ``fused_2hop_backward`` into
+a persistent gradient buffer that it zero-fills every step (train.py:185-251, fused.py:290-296).
+This executor does the same work per step with B200-side plumbing instead of per-call host
+work:
+
+* every buffer (seeds, base seed, out, s1/s2, take arrays, gradient, workspaces) is allocated
+  once, so the whole step is captured as CUDA graphs and replayed with one launch;
+* the base seed is read from device memory by the kernels (``fsa_fused_2hop_fwd_dseed``), so a
+  replay samples a fresh neighbourhood per step exactly like the eager call;
+* the persistent N x D gradient is kept equal to the reference's "zero-filled then scattered"
+  buffer by re-zeroing only the rows written in the previous step, on a side stream that runs
+  concurrently with the (latency-bound) forward; two graphs alternate s2 buffers so the side
+  stream reads the previous step's ids while the forward writes the current ones.
+
+Results are bitwise identical to the eager API (tests/test_gpu_executor.py).
+"""
+
+from __future__ import annotations
+
+from typing import Optional
+
+import torch
+
+from . import _lib
+from .fused import _DTYPE_CODE, _set_device, SampledIndices2
+from .graph import CsrGraph
+
+__all__ = ["Fused2HopStep"]
+
+
+class Fused2HopStep:
+    """One rank's fused 2-hop (k1, k2) forward + replay backward over batches of ``batch``
+    seeds at global positions ``root_offset + [0, batch)``."""
+
+    def __init__(self, graph: CsrGraph, X: torch.Tensor, batch: int, k1: int, k2: int, *,
+                 root_offset: int = 0, use_graph: bool = True, overlap_zero: bool = True):
+        if X.ndim != 2 or X.shape[0] != graph.num_nodes or X.stride(1) != 1:
+            raise ValueError(f"features must be ({graph.num_nodes}, D) row-major")
+        if X.dtype not in _DTYPE_CODE:
+            raise ValueError(f"unsupported feature dtype {X.dtype}")
+        if k1 < 1 or k2 < 1 or batch < 1:
+            raise ValueError("fanouts and batch must be >= 1")
+        self.g, self.X = graph, X
+        self.B, self.k1, self.k2 = int(batch), int(k1), int(k2)
+        self.N, self.D = graph.num_nodes, int(X.shape[1])
+        self.root_offset = int(root_offset)
+        self.device = X.device
+        self.dtype = X.dtype
+        self.code = _DTYPE_CODE[X.dtype]
+        self.use_graph, self.overlap_zero = use_graph, overlap_zero
+        dev = self.device
+        lib = _lib.load()
+        _set_device(dev)
+        B, k1, k2, D, N = self.B, self.k1, self.k2, self.D, self.N
+        self.seeds = torch.zeros(B, dtype=torch.int64, device=dev)
+        self.base_seed = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.grad_out = torch.zeros((B, D), dtype=self.dtype, device=dev)
+        self.out = torch.empty((B, D), dtype=self.dtype, device=dev)
+        self.s1 = torch.empty((B, k1), dtype=torch.int32, device=dev)
+        self.s2 = [torch.full((B, k1, k2), -1, dtype=torch.int32, device=dev) for _ in range(2)]
+        self.t1 = torch.empty(B, dtype=torch.int32, device=dev)
+        self.t2 = torch.empty((B, k1), dtype=torch.int32, device=dev)
+        self.grad = torch.zeros((N, D), dtype=self.dtype, device=dev)
+        self.ws_f = torch.zeros(lib.fsa_ws_bytes(_lib.FSA_OP_FWD2, B, k1, k2, 0), dtype=torch.uint8, device=dev)
+        self.ws_b = torch.zeros(lib.fsa_ws_bytes(_lib.FSA_OP_BWD2, B, k1, k2, N), dtype=torch.uint8, device=dev)
+        self.side = torch.cuda.Stream(device=dev)
+        self.parity = 0
+        self.graphs = [None, None]
+        self.steps_run = 0
+
+    # -- raw launch sequence of one step (eager or under capture) ----------------------------
+    def _launch(self, parity: int) -> None:
+        lib = _lib.load()
+        main = torch.cuda.current_stream(self.device)
+        cur, prev = self.s2[parity], self.s2[1 - parity]
+        zs = self.side if self.overlap_zero else main
+        if self.overlap_zero:
+            zs.wait_stream(main)
+        with torch.cuda.stream(zs):
+            _lib.check(lib.fsa_zero_rows(self.grad.data_ptr(), self.D, self.code, prev.data_ptr(), prev.numel(),
+                                         zs.cuda_stream), "fsa_zero_rows")
+        st = main.cuda_stream
+        _lib.check(lib.fsa_fused_2hop_fwd_dseed(
+            self.g.rowptr.data_ptr(), self.g.col.data_ptr(), self.N, self.X.data_ptr(), self.D, self.X.stride(0),
+            self.code, self.seeds.data_ptr(), self.B, self.root_offset, self.k1, self.k2,
+            self.base_seed.data_ptr(), 1, self.s1.data_ptr(), cur.data_ptr(), self.t1.data_ptr(),
+            self.t2.data_ptr(), self.out.data_ptr(), self.out.stride(0), self.ws_f.data_ptr(), self.ws_f.numel(),
+            st), "fsa_fused_2hop_fwd_dseed")
+        if self.overlap_zero:
+            main.wait_stream(zs)
+        _lib.check(lib.fsa_fused_2hop_bwd(
+            self.grad_out.data_ptr(), self.B, self.D, self.grad_out.stride(0), self.code, self.s1.data_ptr(),
+            cur.data_ptr(), self.k1, self.k2, self.N, self.grad.data_ptr(), 0, None, None, None,
+            self.ws_b.data_ptr(), self.ws_b.numel(), st), "fsa_fused_2hop_bwd")
+
+    def _capture(self, parity: int) -> torch.cuda.CUDAGraph:
+        # warm the launch path once outside capture (device init, function attributes)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self._launch(parity)
+        return g
+
+    def run(self, seeds: Optional[torch.Tensor], base_seed: int, grad_out: Optional[torch.Tensor] = None):
+        """One step.  ``seeds`` (int64 [B], device or pinned host) and ``grad_out`` ([B, D]) are
+        copied into the static buffers (pass None to reuse what is there).  Returns
+        ``(out, SampledIndices2)`` views of the static buffers, valid until the next call."""
+        if seeds is not None:
+            self.seeds.copy_(seeds, non_blocking=True)
+        b = int(base_seed) & 0xFFFFFFFFFFFFFFFF
+        self.base_seed.fill_(b - (1 << 64) if b >= (1 << 63) else b)  # same 64 bits, int64 storage
+        if grad_out is not None:
+            self.grad_out.copy_(grad_out, non_blocking=True)
+        p = self.parity
+        if self.use_graph:
+            if self.steps_run < 2:  # first use of each parity runs eagerly (init, attributes)
+                self._launch(p)
+            else:
+                if self.graphs[p] is None:
+                    self.graphs[p] = self._capture(p)
+                self.graphs[p].replay()
+        else:
+            self._launch(p)
+        self.steps_run += 1
+        self.parity = 1 - p
+        return self.out, SampledIndices2(self.s1, self.s2[p])

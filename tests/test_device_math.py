@@ -182,3 +182,41 @@ def test_rng_mirror_matches_reference_goldens(golden_rng):
     for bound, row in zip(g["ui_bounds"], g["ui"]):
         s = derive_stream(11, 4, 2, 1)
         assert [s.uniform_index(int(bound)) for _ in range(32)] == [int(v) for v in row]
+
+
+def mtab_entry(m):
+    """csrc mtab_entry: FA = floor(frac(2^32/m) 2^64), FB = floor(2^64/m)."""
+    return (((1 << 32) % m) << 64) // m, barrett_recip(m)
+
+
+def frac_q32(x, FA, FB):
+    """Bit-exact model of csrc frac_q32 (32-bit wrapping IMAD / IMAD.HI chain)."""
+    xl, xh = x & M32, x >> 32
+    f = ((xh * (FA & M32)) >> 32) + 4
+    f = (xh * (FA >> 32) + f) & M32
+    f = (((xl * (FB & M32)) >> 32) + f) & M32
+    return (xl * (FB >> 32) + f) & M32
+
+
+def test_fraction_candidate_test_never_misses():
+    """frac(x/m) in 0.32 fixed point + conservative threshold is a superset of x % m < k, and
+    its false-positive rate stays near k/m (the sampler's fast path)."""
+    rng = np.random.default_rng(5)
+    cands = hits = 0
+    n = 60000
+    for i in range(n):
+        m = int(rng.integers(16384, 1 << 21)) if i % 4 else int(rng.integers(2, 1 << 14))
+        k = int(rng.integers(1, 30))
+        if k >= m:
+            continue
+        x = int(rng.integers(0, 2**63)) * 2 + int(rng.integers(0, 2))
+        if i % 5 == 0:
+            x = m * int(rng.integers(0, M64 // m)) + int(rng.integers(0, k))       # true hits
+        elif i % 5 == 1:
+            x = m * int(rng.integers(1, M64 // m)) - int(rng.integers(1, 3))    # frac just below 1
+        FA, FB = mtab_entry(m)
+        c = frac_q32(x, FA, FB) < ((k * (FB >> 32) + k + 6) & M32)
+        assert c or x % m >= k, (x, m, k)
+        cands += c
+        hits += x % m < k
+    assert cands < hits + 0.05 * n
