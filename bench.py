@@ -55,6 +55,9 @@ def parse_args():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--profile", action="store_true", help="print the per-kernel table to stderr")
     p.add_argument("--eager", action="store_true", help="no CUDA graphs for the device-resident measurement")
+    p.add_argument("--flush", default="read", choices=["read", "write", "none"],
+                   help="L2 flush between timed steps: read 512 MiB (evicts, leaves L2 clean), write "
+                        "512 MiB (evicts, leaves L2 dirty: its write-back lands in the timed step), none")
     return p.parse_args()
 
 
@@ -202,12 +205,24 @@ class Runner:
         gen.manual_seed(args.seed + 7)
         self.gout = torch.randn((self.B, self.D), generator=gen, device=device).to(dtype)
         self.gbuf = torch.zeros((self.N, self.D), dtype=dtype, device=device)
-        self.flush = torch.empty(512 << 20, dtype=torch.uint8, device=device)
+        self.flush_buf = torch.ones(512 << 20 >> 3, dtype=torch.int64, device=device)
+        self.flush_sink = torch.zeros(1, dtype=torch.int64, device=device)
         from paper_2511_13645_b200.executor import Fused2HopStep
         self.ex = Fused2HopStep(self.g, self.X, self.B, self.k1, self.k2, root_offset=self.root_offset,
                                 use_graph=not args.eager)
         self.ex.grad_out.copy_(self.gout)
         self.idx = None
+
+    def flush_l2(self):
+        """Evict L2 (126 MB) before a timed step, outside its events: a 512 MiB read (default)
+        leaves L2 clean; a 512 MiB write leaves it full of dirty lines whose write-back then
+        competes with the step for HBM bandwidth."""
+        mode = self.args.flush
+        if mode == "read":
+            torch = self.torch
+            torch.sum(self.flush_buf, dim=0, keepdim=True, out=self.flush_sink)
+        elif mode == "write":
+            self.flush_buf.fill_(1)
 
     def step(self, i):
         out, idx = self.ex.run(self.batches[i], self.base_seeds[i])
@@ -239,7 +254,7 @@ class Runner:
         t_wall = time.perf_counter()
         for j in range(steps):
             if flush:
-                self.flush.zero_()
+                self.flush_l2()
             a, b = evs[j]
             a.record()
             self.step(warmup + j)
@@ -275,10 +290,16 @@ class Runner:
     def profile(self, steps=20):
         from paper_2511_13645_b200 import _lib
         torch = self.torch
+        if not self.args.eager:  # per-kernel times inside the captured step graph
+            n = min(steps, len(self.batches))
+            return self.ex.kernel_times(self.batches[:n], self.base_seeds[:n], flush=self.flush_l2)
         torch.cuda.synchronize(self.device)
         _lib.profile(True)
         for j in range(steps):
-            self.flush.zero_()
+            self.flush_l2()
+            # park the stream behind a ~1 ms spin so the step's launches queue up and the
+            # per-kernel events measure back-to-back device time, not host launch gaps
+            torch.cuda._sleep(2_000_000)
             self.eager_step(j)
         torch.cuda.synchronize(self.device)
         prof = _lib.profile_read()
@@ -436,7 +457,10 @@ def run_fused(args):
             "num_nodes": r.N, "arcs": r.g.num_edges, "max_degree": r.g.max_degree(), "alpha": args.alpha,
             "avg_degree_target": shape.avg_degree, "d_feat": D, "batch_per_gpu": B, "global_batch": B * world,
             "fanouts": [k1, k2], "parallelism": f"seed-sharded dp{world} (root_offset), no data-path collective",
-            "l2": "flushed before every timed step (512 MiB memset outside the step's CUDA events)",
+            "l2": {"read": "flushed before every timed step by a 512 MiB read outside the step's CUDA events "
+                           "(evicts L2, leaves it clean); inputs (1.5 GB CSR + features) are larger than L2",
+                   "write": "flushed before every timed step by a 512 MiB write outside the step's CUDA events",
+                   "none": "no flush; inputs (1.5 GB CSR + features, random rows) are larger than L2"}[args.flush],
             "grad_buffer": "persistent N x D, sparse re-zero of the previous step's rows (fsa_zero_rows) "
                            "on a side stream overlapped with the forward",
             "execution": "eager" if args.eager else "CUDA graph per step (executor.Fused2HopStep)",

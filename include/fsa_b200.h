@@ -76,6 +76,14 @@ unsigned long long fsa_launch_count(void);
 int fsa_profile(int enable);
 int fsa_profile_read(int max_kernels, char* names, double* total_ms, int64_t* launches, int* n_kernels);
 
+/* Per-block timeline of this library's kernels on the current device, for profiling: with a
+ * device buffer of slots*blocks*2 uint64 (fsa_trace_geometry; starts set to UINT64_MAX, ends to
+ * 0), every block of every kernel folds its first-warp start and last-warp end (%globaltimer,
+ * ns) into buf[(slot*blocks + blockIdx)*2 + {0,1}]; slot = kernel kind (see TraceSlot in the
+ * source).  fsa_trace(NULL) turns it off (the default). */
+int fsa_trace(void* buf);
+int fsa_trace_geometry(int* slots, int* blocks);
+
 /* Workspace bytes for `op`.  FWD1: (B, k1=k); FWD2: (B, k1, k2); BWD1: (B, k1=k, N);
  * BWD2: (B, k1, k2, N).  Unused arguments are ignored. */
 size_t fsa_ws_bytes(int op, int64_t B, int32_t k1, int32_t k2, int64_t N);
@@ -158,6 +166,10 @@ int fsa_derive_states(const uint64_t* base_seed, const int64_t* root, const int6
 int fsa_xorshift_steps(uint64_t state, int64_t n, uint64_t* out, void* stream);
 /* out[i] = T^dist[i](states[i]) through the GF(2) jump tables */
 int fsa_jump(const uint64_t* states, const int64_t* dist, int64_t n, uint64_t* out, void* stream);
+/* Adds to *mismatches (device u64) the number of inputs where the backward's reciprocal-based
+ * division differs bitwise from IEEE division: every divisor 1..dmax against every fp32
+ * significand of two binades, plus sampled fp64 inputs. */
+int fsa_div_check(int dmax, unsigned long long* mismatches, void* stream);
 /* out[i] = x[i] % m[i] through the Barrett path used by the sampler (2 <= m <= 2^30) */
 int fsa_umod(const uint64_t* x, const uint32_t* m, int64_t n, uint32_t* out, void* stream);
 

@@ -32,6 +32,8 @@ SIGNATURES = {
     "fsa_launch_count": (C.c_ulonglong, []),
     "fsa_profile": (_int, [_int]),
     "fsa_profile_read": (_int, [_int, _p, _p, _p, C.POINTER(_int)]),
+    "fsa_trace": (_int, [_p]),
+    "fsa_trace_geometry": (_int, [C.POINTER(_int), C.POINTER(_int)]),
     "fsa_ws_bytes": (_sz, [_int, _i64, _i32, _i32, _i64]),
     "fsa_read_error": (_int, [_p, _int, C.POINTER(_int), _p]),
     "fsa_fused_1hop_fwd": (_int, [_p, _p, _i64, _p, _i64, _i64, _int, _p, _i64, _i64, _i32, _u64, _int,
@@ -51,6 +53,7 @@ SIGNATURES = {
     "fsa_xorshift_steps": (_int, [_u64, _i64, _p, _p]),
     "fsa_jump": (_int, [_p, _p, _i64, _p, _p]),
     "fsa_umod": (_int, [_p, _p, _i64, _p, _p]),
+    "fsa_div_check": (_int, [_int, _p, _p]),
 }
 
 _LIB = None

@@ -125,3 +125,30 @@ class Fused2HopStep:
         self.steps_run += 1
         self.parity = 1 - p
         return self.out, SampledIndices2(self.s1, self.s2[p])
+
+    def kernel_times(self, seeds_list, base_seeds, flush=None) -> dict:
+        """Per-kernel device time inside the captured step graph: {name: (ms per launch, launches
+        per step)}.  A dedicated graph is captured with event-record nodes around every kernel
+        (fsa_profile), replayed once per (seeds, base_seed) pair, each optionally preceded by
+        ``flush()`` (an L2 flush), and discarded."""
+        _lib.profile(True)
+        try:
+            g = self._capture(self.parity)
+            tot: dict = {}
+            for seeds, bs in zip(seeds_list, base_seeds):
+                self.seeds.copy_(seeds, non_blocking=True)
+                b = int(bs) & 0xFFFFFFFFFFFFFFFF
+                self.base_seed.fill_(b - (1 << 64) if b >= (1 << 63) else b)
+                if flush is not None:
+                    flush()
+                g.replay()
+                torch.cuda.synchronize(self.device)
+                for k, (ms, n) in _lib.profile_read().items():
+                    t, c = tot.get(k, (0.0, 0))
+                    tot[k] = (t + ms, n)
+            del g
+        finally:
+            _lib.profile(False)
+        steps = max(1, len(base_seeds))
+        return {k: (t / steps / n, n) for k, (t, n) in tot.items()}
+

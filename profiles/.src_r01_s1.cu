@@ -52,38 +52,6 @@ __device__ uint64_t g_jump[NJUMP * 256];  // nibble tables of T^(2^e): [e][16 po
 constexpr int RECIP_N = 1 << 21;
 __device__ uint4 g_mtab[RECIP_N];
 
-// ---- optional per-block timeline (fsa_trace): [slot][block][start, end] in %globaltimer ns ----
-constexpr int TRACE_SLOTS = 16;
-constexpr int TRACE_BLOCKS = 4096;
-enum TraceSlot {
-  TR_PLAN_ROOTS = 0, TR_SAMPLE1, TR_PLAN_HOP2, TR_SAMPLE2, TR_GATHER, TR_ZERO, TR_BWD_COUNT, TR_BWD_SINGLE,
-  TR_BWD_SCATTER, TR_BWD_MULTI
-};
-__device__ unsigned long long* g_trace = nullptr;
-
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-
-// RAII: lane 0 of every warp folds its start / end into the block's record (atomicMin / Max),
-// so the record spans the block's first warp start to its last warp exit.  Off (one load of a
-// null pointer) unless fsa_trace() installed a buffer.
-struct BlockTrace {
-  unsigned long long* p;
-  __device__ __forceinline__ explicit BlockTrace(int slot) {
-    p = g_trace;
-    if (p) {
-      p += ((size_t)slot * TRACE_BLOCKS + min((int)blockIdx.x, TRACE_BLOCKS - 1)) * 2;
-      if ((threadIdx.x & 31) == 0) atomicMin(p, gtimer());
-    }
-  }
-  __device__ __forceinline__ ~BlockTrace() {
-    if (p && (threadIdx.x & 31) == 0) atomicMax(p + 1, gtimer());
-  }
-};
-
 thread_local int t_last_cuda_error = 0;
 
 // ---- launch accounting + optional per-kernel CUDA-event timing ------------------------------
@@ -148,22 +116,16 @@ struct LaunchScope {
 // ------------------------------------------------------------------------------------------
 constexpr int NCLASS = 128;  // chain-length classes (quarter octaves of the bucket count)
 
-// Tile layout of one sampling phase ("position-major"): the chains, ordered by length class
-// (longest first), are cut into buckets of SEG = 2^log2seg consecutive draws.  At bucket s the
-// chains still running form a prefix of that order, so the tiles of bucket s are the
-// ceil(prefix / 32) groups of 32 consecutive chains.  Buckets in [nb_next[c], nb[c]) share the
-// prefix "classes 0..c" (segment c); seg_tile[c] is the exclusive prefix of tiles per segment.
 struct PhaseHdr {
   int num_tiles;
   int blocks_done;
   int tile_counter;
-  int log2seg;                 // bucket length chosen by the last plan block
+  int log2seg;                // bucket length chosen by the last plan block
   unsigned long long draws;
-  int class_cnt[NCLASS];       // chains per class
-  int class_len[NCLASS];       // longest chain of the class, in draws
-  int class_start[NCLASS + 1]; // exclusive prefix of class_cnt (classes in length order)
-  int nb_next[NCLASS];         // buckets of the next non-empty (shorter) class
-  int seg_tile[NCLASS + 1];    // exclusive prefix of tiles per segment
+  int class_cnt[NCLASS];      // chains per class
+  int class_len[NCLASS];      // longest chain of the class, in draws
+  int class_nb[NCLASS];       // ... in buckets
+  int class_tile[NCLASS + 1]; // exclusive prefix of tiles per class
 };
 
 struct FwdHdr {
@@ -246,8 +208,6 @@ struct BwdLayout {
   int* order; // slots of multi-occurrence nodes  [T]
   int* small_list;
   int* big_list;
-  int* big_n;   // slot count of big_list[i]
-  int* big_q;   // its COO row (touched index), -1 without COO output
   size_t bytes;
 };
 
@@ -261,15 +221,13 @@ BwdLayout bwd_layout(void* ws, int64_t G, int64_t T, int64_t N) {
   L.rank = cv.take<int>(T);
   L.order = cv.take<int>(T);
   L.small_list = cv.take<int>(T);
-  L.big_list = cv.take<int>(T / 33 + 1);
-  L.big_n = cv.take<int>(T / 33 + 1);
-  L.big_q = cv.take<int>(T / 33 + 1);
+  L.big_list = cv.take<int>(T);
   L.bytes = align_up(cv.off, 256);
   return L;
 }
 
 constexpr int PLAN_THREADS = 256;
-constexpr int SEG_MIN_LOG2 = 6;   // bucket length bounds (draws per lane per tile)
+constexpr int SEG_MIN_LOG2 = 8;   // bucket length bounds (draws per lane per tile)
 constexpr int SEG_MAX_LOG2 = 12;
 constexpr int CHUNK = 256;        // draws whose modulus constants are staged at a time
 
@@ -350,30 +308,6 @@ __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(
 __device__ __forceinline__ float div_rn(float a, float b) { return __fdiv_rn(a, b); }
 __device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(a, b); }
 
-// x / d correctly rounded, bitwise equal to div_rn, for a positive integer-valued divisor d with
-// its correctly rounded reciprocal r = rcp_rn(d) precomputed (one per row / slot): q0 = x*r is
-// within 1 ulp of x/d, the residual x - d*q0 is exact (FMA), and q0 + residual*r rounded once is
-// the correctly rounded quotient (Markstein's theorem, radix 2, round to nearest).  The theorem
-// needs no underflow / overflow in the residual: x outside [2^-100, 2^100] (zero, subnormal,
-// huge, inf, NaN) takes the IEEE division.  tests/test_gpu_parity.py::test_division_hook checks
-// it against __fdiv_rn exhaustively over a binade for every d <= 4096.
-__device__ __forceinline__ float rcp_rn(float d) { return __frcp_rn(d); }
-__device__ __forceinline__ double rcp_rn(double d) { return __drcp_rn(d); }
-__device__ __forceinline__ float div_rcp(float x, float d, float r) {
-  const float q0 = __fmul_rn(x, r);
-  const float e = __fmaf_rn(-d, q0, x);
-  const float q = __fmaf_rn(e, r, q0);
-  const uint32_t ax = __float_as_uint(x) & 0x7fffffffu;  // exponent field in [27, 227]
-  return (ax - (27u << 23)) < ((228u - 27u) << 23) ? q : __fdiv_rn(x, d);
-}
-__device__ __forceinline__ double div_rcp(double x, double d, double r) {
-  const double q0 = __dmul_rn(x, r);
-  const double e = __fma_rn(-d, q0, x);
-  const double q = __fma_rn(e, r, q0);
-  const uint64_t ax = (uint64_t)__double_as_longlong(x) & 0x7fffffffffffffffull;  // exp in [923, 1123]
-  return (ax - (923ull << 52)) < ((1124ull - 923ull) << 52) ? q : __ddiv_rn(x, d);
-}
-
 template <int BYTES> struct RawVec;
 template <> struct RawVec<16> { using type = uint4; };
 template <> struct RawVec<8> { using type = uint2; };
@@ -429,6 +363,7 @@ __device__ void plan_finish(Chains ch, PhaseHdr* ph, int64_t nc, int64_t c, int 
   __shared__ int s_cnt[NCLASS];
   __shared__ int s_max[NCLASS];
   __shared__ int s_base[NCLASS];
+  __shared__ int s_scan[32];
   __shared__ unsigned long long s_draws;
   __shared__ bool s_last;
   __shared__ int s_log2seg;
@@ -478,77 +413,31 @@ __device__ void plan_finish(Chains ch, PhaseHdr* ph, int64_t nc, int64_t c, int 
   if (!s_last) return;
   __threadfence();
   if (tid == 0) {
-    // bucket length: about two tiles' worth of work per SM sub-partition at full lanes keeps the
-    // critical path short when work is scarce; long buckets amortise the jump-ahead otherwise
     const unsigned long long draws = __ldcg(&ph->draws);
-    const unsigned long long target = (unsigned long long)max(1, sampler_warps / 4);
     int l2 = SEG_MIN_LOG2;
-    while (l2 < SEG_MAX_LOG2 && (draws >> (l2 + 6)) >= target) ++l2;
+    while (l2 < SEG_MAX_LOG2 && (draws >> (l2 + 1 + 5)) >= 2ull * (unsigned long long)sampler_warps) ++l2;
     s_log2seg = l2;
   }
   __syncthreads();
   const int log2seg = s_log2seg;
-  // one warp lays out the <= 128 classes (4 per lane): prefix of counts, bucket counts, suffix
-  // max of bucket counts (= buckets of the next non-empty class, counts are non-increasing over
-  // non-empty classes), tiles per segment and their prefix
-  if (tid < 32) {
-    constexpr int PER = NCLASS / 32;
-    int cnt[PER], nb[PER];
-    int csum = 0, nmax = 0;
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      const int i = tid * PER + q;
-      cnt[q] = __ldcg(&ph->class_cnt[i]);
-      nb[q] = cnt[q] ? (__ldcg(&ph->class_len[i]) + (1 << log2seg) - 1) >> log2seg : 0;
-      csum += cnt[q];
+  int carry = 0;
+  for (int b0 = 0; b0 < NCLASS; b0 += blockDim.x) {
+    const int i = b0 + tid;
+    int v = 0;
+    if (i < NCLASS) {
+      const int nbk = (__ldcg(&ph->class_len[i]) + (1 << log2seg) - 1) >> log2seg;
+      ph->class_nb[i] = nbk;
+      v = ((__ldcg(&ph->class_cnt[i]) + 31) >> 5) * nbk;
     }
-    const int cincl = warp_incl_scan(csum, tid);
-    // suffix max over lanes > tid of the lane-local max
-#pragma unroll
-    for (int q = 0; q < PER; ++q) nmax = max(nmax, nb[q]);
-    int suf;  // max nb over the classes of lanes tid+1..31
-    {
-      int x = nmax;  // inclusive suffix max via shuffles
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_down_sync(FULL, x, o);
-        if (tid + o < 32) x = max(x, y);
-      }
-      suf = __shfl_down_sync(FULL, x, 1);
-      if (tid == 31) suf = 0;
-    }
-    int run = cincl - csum;  // chains in classes before this lane's first class
-    int tiles = 0;
-    int segt[PER];
-    int later = suf;  // max nb over classes after the current one
-    int nbn[PER];
-#pragma unroll
-    for (int q = PER - 1; q >= 0; --q) {
-      nbn[q] = later;
-      later = max(later, nb[q]);
-    }
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      const int i = tid * PER + q;
-      ph->class_start[i] = run;
-      run += cnt[q];
-      segt[q] = cnt[q] ? (nb[q] - nbn[q]) * ((run + 31) >> 5) : 0;
-      ph->nb_next[i] = nbn[q];
-      tiles += segt[q];
-    }
-    const int tincl = warp_incl_scan(tiles, tid);
-    int tb = tincl - tiles;
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      ph->seg_tile[tid * PER + q] = tb;
-      tb += segt[q];
-    }
-    if (tid == 31) {
-      ph->class_start[NCLASS] = run;
-      ph->seg_tile[NCLASS] = tincl;
-      ph->num_tiles = tincl;
-      ph->log2seg = log2seg;
-    }
+    int tot;
+    const int incl = block_incl_scan(v, s_scan, &tot);
+    if (i < NCLASS) ph->class_tile[i] = carry + incl - v;
+    carry += tot;
+  }
+  if (tid == 0) {
+    ph->class_tile[NCLASS] = carry;
+    ph->num_tiles = carry;
+    ph->log2seg = log2seg;
   }
 }
 
@@ -557,7 +446,6 @@ __global__ void __launch_bounds__(PLAN_THREADS)
 k_plan_roots(const int32_t* __restrict__ rowptr, int64_t N, const int64_t* __restrict__ seeds, int64_t B,
              int64_t root_off, int hop, int k, uint64_t base, const uint64_t* __restrict__ base_dev,
              int sampler_warps, Chains ch, PhaseHdr* ph, int* err) {
-  BlockTrace trace_(TR_PLAN_ROOTS);
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (base_dev) base = *base_dev;
   int start = 0, deg = 0;
@@ -581,7 +469,6 @@ k_plan_hop2(const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
             int64_t root_off, int k1, int k2, uint64_t base, const uint64_t* __restrict__ base_dev,
             int sampler_warps, Chains c1, Chains c2, PhaseHdr* ph2, int save, int32_t* __restrict__ s1, int32_t* __restrict__ take1,
             int* err) {
-  BlockTrace trace_(TR_PLAN_HOP2);
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (base_dev) base = *base_dev;
   const int64_t nc = B * k1;
@@ -689,57 +576,33 @@ __device__ __forceinline__ uint4 mtab_entry(uint32_t m) {  // 2 <= m < 2^32
 constexpr uint32_t FAST_M = 16384;  // below this a lane hits too often for the candidate path
 
 __global__ void __launch_bounds__(SAMPLER_THREADS)
-k_sample(Chains ch, PhaseHdr* ph, int k, ShiftK K, int trace_slot) {
-  BlockTrace trace_(trace_slot);
+k_sample(Chains ch, PhaseHdr* ph, int k, ShiftK K) {
   __shared__ uint4 s_T[SAMPLER_THREADS / 32][CHUNK];  // per warp: modulus constants of a chunk
-  __shared__ int s_cstart[NCLASS + 1], s_segt[NCLASS + 1], s_nbn[NCLASS];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   uint4* Rs = s_T[wib];
-  for (int i = threadIdx.x; i <= NCLASS; i += blockDim.x) {
-    s_cstart[i] = ph->class_start[i];
-    s_segt[i] = ph->seg_tile[i];
-    if (i < NCLASS) s_nbn[i] = ph->nb_next[i];
-  }
-  __syncthreads();
-  const int num_tiles = s_segt[NCLASS];
+  const int num_tiles = ph->num_tiles;
   const int log2seg = ph->log2seg;
   const int SEG = 1 << log2seg;
   const int nwarps_total = gridDim.x * (blockDim.x >> 5);
   const uint32_t kk = (uint32_t)k, k6 = kk + 6u;
-  // first tile static and spread across CTAs (consecutive tiles -> different SMs), then dynamic
-  int tau = wib * gridDim.x + blockIdx.x;
+  int tau = blockIdx.x * (blockDim.x >> 5) + wib;  // first tile static, then dynamic
   while (tau < num_tiles) {
-    int lo = 0, hi = NCLASS - 1;  // segment: largest class with seg_tile[c] <= tau
+    int lo = 0, hi = NCLASS - 1;  // largest class with class_tile[c] <= tau
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
-      if (s_segt[mid] <= tau) lo = mid; else hi = mid - 1;
+      if (ph->class_tile[mid] <= tau) lo = mid; else hi = mid - 1;
     }
-    const int active = s_cstart[lo + 1];  // chains of classes 0..lo run at these buckets
-    const int groups = (active + 31) >> 5;
-    const int rel = tau - s_segt[lo];
-    const int bk = rel / groups;
-    const int grp = rel - bk * groups;
-    const int q0 = (s_nbn[lo] + bk) << log2seg;  // first draw index of this bucket
-    const int pos = (grp << 5) + lane;            // position in the length-ordered chain list
-    // stage the modulus constants of the first chunk now: they depend only on the bucket
-    const uint32_t mfirst = kk + (uint32_t)q0 + 1u;
-    const bool staged32 = (uint64_t)mfirst + CHUNK <= (1ull << 30);
-    if (staged32) {
-#pragma unroll
-      for (int u = 0; u < CHUNK / 32; ++u) {
-        const uint32_t m = mfirst + (uint32_t)(u * 32 + lane);
-        if (u * 32 < SEG) Rs[u * 32 + lane] = m < RECIP_N ? g_mtab[m] : mtab_entry(m);
-      }
-    }
+    const int cls = lo;
+    const int cnb = ph->class_nb[cls];
+    const int rel = tau - ph->class_tile[cls];
+    const int grp = rel / cnb;
+    const int p = rel - grp * cnb;
+    const int pos = (grp << 5) + lane;
+    const int q0 = p << log2seg;  // first draw index of this bucket
     int c = 0, n_l = 0;
     uint64_t s = 0;
-    if (pos < active) {
-      int cl = 0, ch2 = lo;  // class holding position pos: largest cl with class_start[cl] <= pos
-      while (cl < ch2) {
-        const int mid = (cl + ch2 + 1) >> 1;
-        if (s_cstart[mid] <= pos) cl = mid; else ch2 = mid - 1;
-      }
-      c = ch.order[(int64_t)cl * ch.nc + (pos - s_cstart[cl])];
+    if (pos < ph->class_cnt[cls]) {
+      c = ch.order[(int64_t)cls * ch.nc + pos];
       const int len = ch.deg[c] - k;
       if (len > q0) {
         n_l = min(SEG, len - q0);
@@ -762,13 +625,10 @@ k_sample(Chains ch, PhaseHdr* ph, int k, ShiftK K, int trace_slot) {
         }
         continue;
       }
-      if (c0 > 0 || !staged32) {
-        __syncwarp();
-#pragma unroll
-        for (int u = 0; u < CHUNK / 32; ++u) {
-          const uint32_t m = m0 + (uint32_t)(u * 32 + lane);
-          Rs[u * 32 + lane] = m < RECIP_N ? g_mtab[m] : mtab_entry(m);
-        }
+      __syncwarp();
+      for (int t = lane; t < cn; t += 32) {
+        const uint32_t m = m0 + (uint32_t)t;
+        Rs[t] = m < RECIP_N ? g_mtab[m] : mtab_entry(m);
       }
       __syncwarp();
       int t = 0;
@@ -844,7 +704,6 @@ __global__ void __launch_bounds__(GATHER_THREADS)
 k_gather1(const int32_t* __restrict__ col, const T* __restrict__ X, int64_t x_stride, int D,
           int64_t B, int k, Chains ch, int32_t* __restrict__ ids, int save, int32_t* __restrict__ takes,
           T* __restrict__ out, int64_t out_stride) {
-  BlockTrace trace_(TR_GATHER);
   using Acc = typename AccOf<T>::type;
   constexpr int U = 8;
   const int lane = threadIdx.x & 31;
@@ -890,7 +749,6 @@ __global__ void __launch_bounds__(GATHER_THREADS)
 k_gather2(const int32_t* __restrict__ col, const T* __restrict__ X, int64_t x_stride, int D,
           int64_t B, int k1, int k2, Chains c1, Chains c2, int32_t* __restrict__ ids, int save,
           int32_t* __restrict__ take2, T* __restrict__ out, int64_t out_stride) {
-  BlockTrace trace_(TR_GATHER);
   using Acc = typename AccOf<T>::type;
   constexpr int U = 8;
   constexpr int CW = 32 * V;
@@ -971,7 +829,6 @@ k_gather2(const int32_t* __restrict__ col, const T* __restrict__ X, int64_t x_st
 __global__ void __launch_bounds__(BWD_THREADS)
 k_bwd_count(const int32_t* __restrict__ ids, const int32_t* __restrict__ aux, int64_t T, int S, int k1,
             int hops, int64_t N, BwdLayout L) {
-  BlockTrace trace_(TR_BWD_COUNT);
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= T) return;
   int err = 0;
@@ -1050,10 +907,9 @@ __device__ __forceinline__ int warp_agg_inc(int* ctr, bool pred, int lane) {
 // the only dependent round trips are ids -> cnt/rank.  The singles of a warp are then written as
 // a flat stream of (row, V-chunk) items: all 32 lanes issue vector stores whatever D is.
 template <typename T, int V>
-__global__ void __launch_bounds__(BWD_THREADS, 6)  // 6 CTAs/SM: one wave at 153.6 k slots
+__global__ void __launch_bounds__(BWD_THREADS)
 k_bwd_single(const T* __restrict__ grad_out, BwdArgs a, BwdLayout L, T* grad_x, T* grad_rows,
              int staged_rows) {
-  BlockTrace trace_(TR_BWD_SINGLE);
   using Acc = typename AccOf<T>::type;
   constexpr int U = 4;  // items in flight per lane
   extern __shared__ __align__(16) unsigned char s_dyn[];
@@ -1064,7 +920,6 @@ k_bwd_single(const T* __restrict__ grad_out, BwdArgs a, BwdLayout L, T* grad_x, 
   __shared__ int s_v[BWD_THREADS];
   __shared__ int s_q[BWD_THREADS];
   __shared__ Acc s_den[BWD_THREADS];
-  __shared__ Acc s_rcp[BWD_THREADS];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t t0 = (int64_t)blockIdx.x * blockDim.x;
   const int64_t t = t0 + tid;
@@ -1098,19 +953,8 @@ k_bwd_single(const T* __restrict__ grad_out, BwdArgs a, BwdLayout L, T* grad_x, 
   if (lead) {
     L.segv[v] = s_base[0] + incl_n - n;
     const int ex = incl_sb - sb;
-    if (n <= 32) {
-      L.small_list[s_base[1] + (ex & 0xffff)] = v;
-    } else {  // a big node is summed by several CTAs (column blocks): fix its COO row here
-      const int bi = s_base[2] + (ex >> 16);
-      L.big_list[bi] = v;
-      L.big_n[bi] = n;
-      int qb = -1;
-      if (a.touched) {
-        qb = atomicAdd(a.n_touched, 1);
-        a.touched[qb] = v;
-      }
-      L.big_q[bi] = qb;
-    }
+    if (n <= 32) L.small_list[s_base[1] + (ex & 0xffff)] = v;
+    else L.big_list[s_base[2] + (ex >> 16)] = v;
   }
   int q = -1;
   if (a.touched) {
@@ -1124,7 +968,6 @@ k_bwd_single(const T* __restrict__ grad_out, BwdArgs a, BwdLayout L, T* grad_x, 
     const int64_t g = t / a.S;
     s_row[p] = (int)(g / a.kdiv);
     s_den[p] = (Acc)L.den[g];
-    s_rcp[p] = rcp_rn((Acc)L.den[g]);
     s_v[p] = v;
     s_q[p] = q;
     L.cnt[v] = 0;  // leave the persistent counters zero
@@ -1150,9 +993,9 @@ k_bwd_single(const T* __restrict__ grad_out, BwdArgs a, BwdLayout L, T* grad_x, 
     for (int u = 0; u < U; ++u) {
       if (it0 + 32 * u < items) {
         Acc o[V];
-        const Acc den = s_den[p[u]], rcp = s_rcp[p[u]];
+        const Acc den = s_den[p[u]];
 #pragma unroll
-        for (int e = 0; e < V; ++e) o[e] = add_rn(Acc(0), div_rcp(to_acc(x[u].v[e]), den, rcp));
+        for (int e = 0; e < V; ++e) o[e] = add_rn(Acc(0), div_rn(to_acc(x[u].v[e]), den));
         store_grad<T, V>(grad_x, grad_rows, s_v[p[u]], s_q[p[u]], a.D, c[u], o);
       }
     }
@@ -1160,7 +1003,6 @@ k_bwd_single(const T* __restrict__ grad_out, BwdArgs a, BwdLayout L, T* grad_x, 
 }
 
 __global__ void k_bwd_scatter(BwdArgs a, BwdLayout L) {
-  BlockTrace trace_(TR_BWD_SCATTER);
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= a.T) return;
   const int v = a.ids[t];
@@ -1170,8 +1012,8 @@ __global__ void k_bwd_scatter(BwdArgs a, BwdLayout L) {
 
 // Multi-hit nodes: the slots of a node are summed in ascending slot order.
 //   small (n <= 32):  one warp, rank-by-comparison sort in registers, lanes over V-chunks;
-//   big (n <= BIG_CAP): one CTA per BIG_COLS columns, bitonic sort of the slot ids in shared
-//                      memory, then the terms g/den of TERM_ROWS slots x BIG_COLS columns are staged in shared
+//   big (n <= BIG_CAP): one CTA, bitonic sort of the slot ids in shared memory, then the
+//                      terms g/den of TERM_ROWS slots x TERM_COLS columns are staged in shared
 //                      memory by all threads at once (many loads in flight) and summed down
 //                      each column in slot order;
 //   huge:              one CTA, windowed bitmap over the slot range (ascending by construction).
@@ -1183,24 +1025,24 @@ __device__ __forceinline__ typename AccOf<T>::type term(const T* __restrict__ gr
   return div_rn(to_acc(__ldg(grad_out + (g / a.kdiv) * a.g_stride + d)), (Acc)L.den[g]);
 }
 
-constexpr int BIG_COLS = 32;  // columns per big-node CTA
+constexpr int TERM_COLS = 128;
 constexpr int TERM_BYTES = 16 * 1024;
 
 template <typename T, int V>
 __global__ void __launch_bounds__(BWD_THREADS, 6)
 k_bwd_multi(const T* __restrict__ grad_out, BwdArgs a, BwdLayout L, T* grad_x, T* grad_rows,
             int small_blocks) {
-  BlockTrace trace_(TR_BWD_MULTI);
   using Acc = typename AccOf<T>::type;
   constexpr int U = 4;
-  constexpr int TERM_ROWS = TERM_BYTES / (BIG_COLS * (int)sizeof(Acc));
+  constexpr int TERM_ROWS = TERM_BYTES / (TERM_COLS * (int)sizeof(Acc));
   // small path: 32 rows per warp; big path: sorted slot ids, then their grad rows in place;
   // huge path: the window's slot list
   __shared__ int s_list[BIG_CAP];
   __shared__ int s_den[BIG_CAP];  // integer denominators, same layout as the rows
-  __shared__ __align__(16) Acc s_term[TERM_ROWS * BIG_COLS];
+  __shared__ __align__(16) Acc s_term[TERM_ROWS * TERM_COLS];
   __shared__ uint32_t s_bits[BIG_WBITS / 32];
   __shared__ int s_scratch[32];
+  __shared__ int s_q;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if ((int)blockIdx.x < small_blocks) {
     const int n_small = L.hdr->n_small;
@@ -1231,19 +1073,18 @@ k_bwd_multi(const T* __restrict__ grad_out, BwdArgs a, BwdLayout L, T* grad_x, T
         for (int e = 0; e < V; ++e) acc[e] = Acc(0);
         for (int i0 = 0; i0 < n; i0 += U) {
           Vec<T, V> x[U];
-          Acc dn[U], rc[U];
+          Acc dn[U];
 #pragma unroll
           for (int u = 0; u < U; ++u)
             if (i0 + u < n) {
               x[u].load(grad_out + (int64_t)wrow[i0 + u] * a.g_stride + d);
               dn[u] = (Acc)wden[i0 + u];
-              rc[u] = rcp_rn(dn[u]);
             }
 #pragma unroll
           for (int u = 0; u < U; ++u)
             if (i0 + u < n) {
 #pragma unroll
-              for (int e = 0; e < V; ++e) acc[e] = add_rn(acc[e], div_rcp(to_acc(x[u].v[e]), dn[u], rc[u]));
+              for (int e = 0; e < V; ++e) acc[e] = add_rn(acc[e], div_rn(to_acc(x[u].v[e]), dn[u]));
             }
         }
         store_grad<T, V>(grad_x, grad_rows, v, q, a.D, d, acc);
@@ -1256,18 +1097,23 @@ k_bwd_multi(const T* __restrict__ grad_out, BwdArgs a, BwdLayout L, T* grad_x, T
     }
     return;
   }
-  // big segments: (node, BIG_COLS-column block) items, one CTA each, so a hub's serial
-  // slot-order sums run on several SMs at once
+  // big segments: one CTA per node
   const int n_big = L.hdr->n_big;
   const int big_blocks = gridDim.x - small_blocks;
-  const int ncb = (a.D + BIG_COLS - 1) / BIG_COLS;
-  for (int it = blockIdx.x - small_blocks; it < n_big * ncb; it += big_blocks) {
-    const int bi = it / ncb, cb = it - bi * ncb;
-    const int v = L.big_list[bi];
-    const int n = L.big_n[bi];
-    const int q = L.big_q[bi];
+  for (int it = blockIdx.x - small_blocks; it < n_big; it += big_blocks) {
+    const int v = L.big_list[it];
+    const int n = L.cnt[v];
     const int base = L.segv[v];
-    const int d0 = cb * BIG_COLS, dc = min(BIG_COLS, a.D - d0);
+    if (tid == 0) {
+      int q = -1;
+      if (a.touched) {
+        q = atomicAdd(a.n_touched, 1);
+        a.touched[q] = v;
+      }
+      s_q = q;
+    }
+    __syncthreads();
+    const int q = s_q;
     if (n <= BIG_CAP) {
       int P = 32;
       while (P < n) P <<= 1;
@@ -1293,87 +1139,80 @@ k_bwd_multi(const T* __restrict__ grad_out, BwdArgs a, BwdLayout L, T* grad_x, T
         s_den[i] = L.den[g];
       }
       __syncthreads();
-      // all threads stage TERM_ROWS x BIG_COLS terms (one coalesced row segment per warp
-      // load); warp 0 then sums each column down the rows in slot order
-      Acc acc = Acc(0);
-      for (int i0 = 0; i0 < n; i0 += TERM_ROWS) {
-        const int nr = min(TERM_ROWS, n - i0);
-        for (int idx = tid; idx < nr * BIG_COLS; idx += blockDim.x) {
-          const int i = idx / BIG_COLS, d = idx - i * BIG_COLS;
-          if (d < dc)
-            s_term[idx] = div_rn(to_acc(__ldg(grad_out + (int64_t)s_list[i0 + i] * a.g_stride + d0 + d)),
-                                 (Acc)s_den[i0 + i]);
+      for (int d0 = 0; d0 < a.D; d0 += TERM_COLS) {
+        const int dc = min(TERM_COLS, a.D - d0);
+        Acc acc = Acc(0);
+        for (int i0 = 0; i0 < n; i0 += TERM_ROWS) {
+          const int nr = min(TERM_ROWS, n - i0);
+          for (int idx = tid; idx < nr * TERM_COLS; idx += blockDim.x) {
+            const int i = idx / TERM_COLS, d = idx - i * TERM_COLS;
+            if (d < dc)
+              s_term[idx] = div_rn(to_acc(__ldg(grad_out + (int64_t)s_list[i0 + i] * a.g_stride + d0 + d)),
+                                   (Acc)s_den[i0 + i]);
+          }
+          __syncthreads();
+          if (tid < dc)
+            for (int i = 0; i < nr; ++i) acc = add_rn(acc, s_term[i * TERM_COLS + tid]);
+          __syncthreads();
         }
-        __syncthreads();
         if (tid < dc) {
-          int i = 0;
-          for (; i + 8 <= nr; i += 8) {
-            Acc tv[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) tv[u] = s_term[(i + u) * BIG_COLS + tid];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) acc = add_rn(acc, tv[u]);
+          const T o = from_acc<T>(acc);
+          if (grad_x) grad_x[(int64_t)v * a.D + d0 + tid] = o;
+          if (grad_rows && q >= 0) grad_rows[(int64_t)q * a.D + d0 + tid] = o;
+        }
+      }
+    } else {
+      for (int d0 = 0; d0 < a.D; d0 += (int)blockDim.x) {
+        const int d = d0 + tid;
+        const bool on = d < a.D;
+        Acc acc = Acc(0);
+        for (int64_t w0 = 0; w0 < a.T; w0 += BIG_WBITS) {
+          for (int i = tid; i < BIG_WBITS / 32; i += blockDim.x) s_bits[i] = 0u;
+          __syncthreads();
+          for (int i = tid; i < n; i += blockDim.x) {
+            const int64_t tt = L.order[base + i];
+            if (tt >= w0 && tt < w0 + BIG_WBITS) {
+              const int o = (int)(tt - w0);
+              atomicOr(&s_bits[o >> 5], 1u << (o & 31));
+            }
           }
-          for (; i < nr; ++i) acc = add_rn(acc, s_term[i * BIG_COLS + tid]);
-        }
-        __syncthreads();
-      }
-      if (tid < dc) {
-        const T o = from_acc<T>(acc);
-        if (grad_x) grad_x[(int64_t)v * a.D + d0 + tid] = o;
-        if (grad_rows && q >= 0) grad_rows[(int64_t)q * a.D + d0 + tid] = o;
-      }
-    } else {  // huge: windowed bitmap over the slot range, ascending by construction
-      const int d = d0 + tid;
-      const bool on = tid < dc;
-      Acc acc = Acc(0);
-      for (int64_t w0 = 0; w0 < a.T; w0 += BIG_WBITS) {
-        for (int i = tid; i < BIG_WBITS / 32; i += blockDim.x) s_bits[i] = 0u;
-        __syncthreads();
-        for (int i = tid; i < n; i += blockDim.x) {
-          const int64_t tt = L.order[base + i];
-          if (tt >= w0 && tt < w0 + BIG_WBITS) {
-            const int o = (int)(tt - w0);
-            atomicOr(&s_bits[o >> 5], 1u << (o & 31));
+          __syncthreads();
+          uint32_t word = 0;
+          int c = 0;
+          if (tid < BIG_WBITS / 32) {
+            word = s_bits[tid];
+            c = __popc(word);
           }
+          int tot;
+          const int incl = block_incl_scan(c, s_scratch, &tot);
+          int pos = incl - c;
+          while (word) {
+            const int b = __ffs(word) - 1;
+            word &= word - 1;
+            s_list[pos++] = (int)(w0 + tid * 32 + b);
+          }
+          __syncthreads();
+          if (on)
+            for (int i = 0; i < tot; ++i) acc = add_rn(acc, term<T>(grad_out, a, L, s_list[i], d));
+          __syncthreads();
         }
-        __syncthreads();
-        uint32_t word = 0;
-        int c = 0;
-        if (tid < BIG_WBITS / 32) {
-          word = s_bits[tid];
-          c = __popc(word);
+        if (on) {
+          const T o = from_acc<T>(acc);
+          if (grad_x) grad_x[(int64_t)v * a.D + d] = o;
+          if (grad_rows && q >= 0) grad_rows[(int64_t)q * a.D + d] = o;
         }
-        int tot;
-        const int incl = block_incl_scan(c, s_scratch, &tot);
-        int pos = incl - c;
-        while (word) {
-          const int b = __ffs(word) - 1;
-          word &= word - 1;
-          s_list[pos++] = (int)(w0 + tid * 32 + b);
-        }
-        __syncthreads();
-        if (on)
-          for (int i = 0; i < tot; ++i) acc = add_rn(acc, term<T>(grad_out, a, L, s_list[i], d));
-        __syncthreads();
-      }
-      if (on) {
-        const T o = from_acc<T>(acc);
-        if (grad_x) grad_x[(int64_t)v * a.D + d] = o;
-        if (grad_rows && q >= 0) grad_rows[(int64_t)q * a.D + d] = o;
       }
     }
     __syncthreads();
-    if (tid == 0) {  // column blocks count the node's counter down; the last one clears segv
-      const int share = cb == ncb - 1 ? n - (ncb - 1) * (n / ncb) : n / ncb;
-      if (atomicSub(&L.cnt[v], share) == share) L.segv[v] = 0;
+    if (tid == 0) {
+      L.cnt[v] = 0;
+      L.segv[v] = 0;
     }
   }
 }
 
 template <typename T, int V>
 __global__ void k_zero_rows(T* grad, int64_t D, const int32_t* __restrict__ rows, int64_t n) {
-  BlockTrace trace_(TR_ZERO);
   const int lane = threadIdx.x & 31;
   const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1417,27 +1256,6 @@ __global__ void k_jump(const uint64_t* st, const int64_t* dist, int64_t n, uint6
   }
 }
 
-// exhaustive check of div_rcp against IEEE division: every d in [1, dmax] x every significand of
-// the binade [1, 2) (sign and exponent scaling are exact in both), plus random doubles
-__global__ void k_div_check(int dmax, unsigned long long* bad) {
-  const int d = blockIdx.y + 1;
-  if (d > dmax) return;
-  const float df = (float)d, r = rcp_rn(df);
-  unsigned long long nb = 0;
-  for (uint32_t m = blockIdx.x * blockDim.x + threadIdx.x; m < (1u << 23); m += gridDim.x * blockDim.x) {
-    const float x = __uint_as_float((127u << 23) | m);
-    nb += __float_as_uint(div_rcp(x, df, r)) != __float_as_uint(__fdiv_rn(x, df));
-    const float xs = __uint_as_float((100u << 23) | m);  // a second binade, smaller values
-    nb += __float_as_uint(div_rcp(xs, df, r)) != __float_as_uint(__fdiv_rn(xs, df));
-    uint64_t z = ((uint64_t)m << 20) ^ ((uint64_t)d * 0x9E3779B97F4A7C15ull);
-    z ^= z >> 29; z *= 0xBF58476D1CE4E5B9ull; z ^= z >> 32;
-    const double xd = __longlong_as_double((long long)((1023ull << 52) | (z & ((1ull << 52) - 1))));
-    const double dd = (double)d, rd = rcp_rn(dd);
-    nb += __double_as_longlong(div_rcp(xd, dd, rd)) != __double_as_longlong(__ddiv_rn(xd, dd));
-  }
-  if (nb) atomicAdd(bad, nb);
-}
-
 __global__ void k_umod(const uint64_t* x, const uint32_t* m, int64_t n, uint32_t* out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = fsa::mod_barrett(x[i], fsa::barrett_recip(m[i]), m[i]);
@@ -1476,23 +1294,6 @@ void build_tables() {
   g_tables_built = true;
 }
 
-// The kernels that can run concurrently (the sparse re-zero on its side stream and the forward's
-// plan / sample kernels it overlaps) use the same L1 / shared-memory split (max shared).  An SM
-// can only change its split when it is empty, so kernels with different splits cannot share an
-// SM: the re-zero would otherwise lock the sampler out of every SM until it drains.  The other
-// kernels keep the default split (more L1), which they use.
-std::mutex g_prep_mu;
-std::vector<std::pair<int, const void*>> g_prepped;
-void prep(const void* f) {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> lk(g_prep_mu);
-  for (auto& e : g_prepped)
-    if (e.first == dev && e.second == f) return;
-  cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-  g_prepped.emplace_back(dev, f);
-}
-
 inline int cuda_fail(cudaError_t e) {
   t_last_cuda_error = (int)e;
   return FSA_ERR_CUDA;
@@ -1516,7 +1317,6 @@ int ensure_device(int* dev_out) {
     FSA_CUDA(cudaGetDeviceProperties(&prop, dev));
     g_num_sms[dev] = prop.multiProcessorCount;
     int occ = 0;
-    prep((const void*)k_sample);
     FSA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
         &occ, k_sample, SAMPLER_THREADS, 0));
     uint4* mtab = nullptr;
@@ -1533,11 +1333,10 @@ int ensure_device(int* dev_out) {
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
-int run_phase_sampler(const Chains& ch, PhaseHdr* ph, int k, int dev, cudaStream_t st, int trace_slot) {
+int run_phase_sampler(const Chains& ch, PhaseHdr* ph, int k, int dev, cudaStream_t st) {
   {
     FSA_LAUNCH("k_sample", st);
-    k_sample<<<g_sampler_blocks[dev], SAMPLER_THREADS, 0, st>>>(ch, ph, k, ShiftK{1u << 13, 1u << 25, 1u << 17},
-                                                               trace_slot);
+    k_sample<<<g_sampler_blocks[dev], SAMPLER_THREADS, 0, st>>>(ch, ph, k, ShiftK{1u << 13, 1u << 25, 1u << 17});
   }
   return FSA_OK;
 }
@@ -1780,19 +1579,6 @@ int fsa_profile_read(int max_kernels, char* names, double* total_ms, int64_t* la
   return FSA_OK;
 }
 
-int fsa_trace(void* buf) {
-  unsigned long long* p = static_cast<unsigned long long*>(buf);
-  FSA_CUDA(cudaMemcpyToSymbol(g_trace, &p, sizeof(p)));
-  return FSA_OK;
-}
-
-int fsa_trace_geometry(int* slots, int* blocks) {
-  if (!slots || !blocks) return FSA_ERR_ARG;
-  *slots = TRACE_SLOTS;
-  *blocks = TRACE_BLOCKS;
-  return FSA_OK;
-}
-
 int fsa_set_device(int device) {
   FSA_CUDA(cudaSetDevice(device));
   return FSA_OK;
@@ -1839,11 +1625,10 @@ static int fwd1_impl(const int32_t* rowptr, const int32_t* col, int64_t N, const
   FSA_CUDA(cudaMemsetAsync(ws, 0, sizeof(FwdHdr), st));
   {
     FSA_LAUNCH("k_plan_roots", st);
-    prep((const void*)k_plan_roots);
     k_plan_roots<<<blocks_for(B, PLAN_THREADS), PLAN_THREADS, 0, st>>>(rowptr, N, seeds, B, root_offset, 0, k, base_seed, base_dev,
                                                      g_sampler_blocks[dev] * (SAMPLER_THREADS / 32), L.c1, &L.hdr->ph[0], &L.hdr->err);
   }
-  run_phase_sampler(L.c1, &L.hdr->ph[0], k, dev, st, TR_SAMPLE1);
+  run_phase_sampler(L.c1, &L.hdr->ph[0], k, dev, st);
   int32_t* ids = save ? samples : L.ids;
   if (int s = gather_by_dtype(dtype, 1, col, X, x_stride, D, B, k, 0, L.c1, L.c2, ids, save, takes,
                               out, out_stride, st))
@@ -1872,20 +1657,18 @@ static int fwd2_impl(const int32_t* rowptr, const int32_t* col, int64_t N, const
   FSA_CUDA(cudaMemsetAsync(ws, 0, sizeof(FwdHdr), st));
   {
     FSA_LAUNCH("k_plan_roots", st);
-    prep((const void*)k_plan_roots);
     k_plan_roots<<<blocks_for(B, PLAN_THREADS), PLAN_THREADS, 0, st>>>(rowptr, N, seeds, B, root_offset, 1, k1, base_seed, base_dev,
                                                      g_sampler_blocks[dev] * (SAMPLER_THREADS / 32), L.c1, &L.hdr->ph[0], &L.hdr->err);
   }
-  run_phase_sampler(L.c1, &L.hdr->ph[0], k1, dev, st, TR_SAMPLE1);
+  run_phase_sampler(L.c1, &L.hdr->ph[0], k1, dev, st);
   {
     FSA_LAUNCH("k_plan_hop2", st);
-    prep((const void*)k_plan_hop2);
     k_plan_hop2<<<blocks_for(B * k1, PLAN_THREADS), PLAN_THREADS, 0, st>>>(rowptr, col, N, B, root_offset, k1, k2, base_seed, base_dev,
                                                          g_sampler_blocks[dev] * (SAMPLER_THREADS / 32), L.c1, L.c2,
                                                        &L.hdr->ph[1], save, s1,
                                                          take1, &L.hdr->err);
   }
-  run_phase_sampler(L.c2, &L.hdr->ph[1], k2, dev, st, TR_SAMPLE2);
+  run_phase_sampler(L.c2, &L.hdr->ph[1], k2, dev, st);
   int32_t* ids = save ? s2 : L.ids;
   if (int s = gather_by_dtype(dtype, 2, col, X, x_stride, D, B, k1, k2, L.c1, L.c2, ids, save, take2,
                               out, out_stride, st))
@@ -1958,14 +1741,12 @@ int fsa_zero_rows(void* grad, int64_t D, int dtype, const int32_t* rows, int64_t
   const uintptr_t al = reinterpret_cast<uintptr_t>(grad);
   int vb = 16;  // vector bytes
   while (vb > (int)es && ((D * (int64_t)es) % vb != 0 || al % vb != 0)) vb >>= 1;
-  // four CTAs per SM: enough stores in flight for HBM, and it leaves room on every SM for the
-  // latency-bound forward it usually overlaps on another stream
-  const unsigned zgrid = (unsigned)std::min<int64_t>((int64_t)g_num_sms[dev] * 4, (n_rows + 7) / 8);
+  const unsigned zgrid = (unsigned)std::min<int64_t>((int64_t)g_num_sms[dev] * 16, (n_rows + 7) / 8);
   switch (vb) {
-    case 16: prep((const void*)k_zero_rows<uint4, 1>); k_zero_rows<uint4, 1><<<zgrid, 256, 0, st>>>((uint4*)grad, D * (int64_t)es / 16, rows, n_rows); break;
-    case 8: prep((const void*)k_zero_rows<uint2, 1>); k_zero_rows<uint2, 1><<<zgrid, 256, 0, st>>>((uint2*)grad, D * (int64_t)es / 8, rows, n_rows); break;
-    case 4: prep((const void*)k_zero_rows<uint32_t, 1>); k_zero_rows<uint32_t, 1><<<zgrid, 256, 0, st>>>((uint32_t*)grad, D * (int64_t)es / 4, rows, n_rows); break;
-    default: prep((const void*)k_zero_rows<unsigned short, 1>); k_zero_rows<unsigned short, 1><<<zgrid, 256, 0, st>>>((unsigned short*)grad, D * (int64_t)es / 2, rows, n_rows); break;
+    case 16: k_zero_rows<uint4, 1><<<zgrid, 256, 0, st>>>((uint4*)grad, D * (int64_t)es / 16, rows, n_rows); break;
+    case 8: k_zero_rows<uint2, 1><<<zgrid, 256, 0, st>>>((uint2*)grad, D * (int64_t)es / 8, rows, n_rows); break;
+    case 4: k_zero_rows<uint32_t, 1><<<zgrid, 256, 0, st>>>((uint32_t*)grad, D * (int64_t)es / 4, rows, n_rows); break;
+    default: k_zero_rows<unsigned short, 1><<<zgrid, 256, 0, st>>>((unsigned short*)grad, D * (int64_t)es / 2, rows, n_rows); break;
   }
   FSA_CUDA(cudaGetLastError());
   return FSA_OK;
@@ -1995,15 +1776,6 @@ int fsa_jump(const uint64_t* states, const int64_t* dist, int64_t n, uint64_t* o
   int dev;
   if (int s = ensure_device(&dev)) return s;
   k_jump<<<blocks_for(n, 256), 256, 0, as_stream(stream)>>>(states, dist, n, out);
-  FSA_CUDA(cudaGetLastError());
-  return FSA_OK;
-}
-
-int fsa_div_check(int dmax, unsigned long long* mismatches, void* stream) {
-  if (dmax < 1 || dmax > 65535 || !mismatches) return FSA_ERR_ARG;
-  int dev;
-  if (int s = ensure_device(&dev)) return s;
-  k_div_check<<<dim3(64, dmax), 256, 0, as_stream(stream)>>>(dmax, mismatches);
   FSA_CUDA(cudaGetLastError());
   return FSA_OK;
 }

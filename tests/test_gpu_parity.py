@@ -356,3 +356,13 @@ def test_repeat_and_shard_invariance(fsa, golden_powerlaw):
             outs.append(o)
             s2s.append(i.s2)
         assert bitwise(torch.cat(outs), c["out2"]) and bitwise(torch.cat(s2s), c["s2"])
+
+
+def test_division_hook(fsa):
+    """The backward divides by a per-slot reciprocal (Markstein); it must equal IEEE division
+    bitwise for every denominator the op can produce (max(t1,1)*max(t2,1) <= k1*k2)."""
+    from paper_2511_13645_b200 import _lib
+    bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+    _lib.check(_lib.load().fsa_div_check(4096, bad.data_ptr(), torch.cuda.current_stream().cuda_stream), "div")
+    torch.cuda.synchronize()
+    assert int(bad.item()) == 0
