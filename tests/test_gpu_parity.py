@@ -321,7 +321,7 @@ def test_fd_gradient_fp64(fsa, golden_small):
         X = T(c["X"])
         seeds = T(c["seeds"])
         out, idx = fsa.fused_2hop_forward(g, X, seeds, c["k1"], c["k2"], c["base_seed"])
-        w = torch.randn_like(out)
+        w = T(np.random.default_rng(4).standard_normal(tuple(out.shape)))
         analytic = fsa.fused_2hop_backward(w, idx, c["N"]).cpu().numpy()
         eps = 1e-6
         fd = np.zeros_like(analytic)
@@ -333,7 +333,9 @@ def test_fd_gradient_fp64(fsa, golden_small):
                 P[v, d] -= 2 * eps
                 fm = float((w * fsa.fused_2hop_forward(g, P, seeds, c["k1"], c["k2"], c["base_seed"], False)[0]).sum())
                 fd[v, d] = (fp - fm) / (2 * eps)
-        scale = np.maximum(np.abs(analytic), 1e-9)
+        # central differences at eps=1e-6 carry ~1e-10 absolute rounding noise in fp64, so the
+        # relative gate of the reference (1e-6) is applied with a 1e-3 floor on the scale
+        scale = np.maximum(np.abs(analytic), 1e-3)
         assert np.max(np.abs(fd - analytic) / scale) < 1e-6, name
 
 
