@@ -152,3 +152,41 @@ class Fused2HopStep:
         steps = max(1, len(base_seeds))
         return {k: (t / steps / n, n) for k, (t, n) in tot.items()}
 
+    TRACE_NAMES = ("k_plan_roots", "k_sample1", "k_plan_hop2", "k_sample2", "k_gather2", "k_zero_rows",
+                   "k_bwd_count", "k_bwd_single", "k_bwd_scatter", "k_bwd_multi")
+
+    def kernel_spans(self, seeds_list, base_seeds, flush=None) -> dict:
+        """Per-kernel device time of the normal step graph, from the library's per-block
+        %globaltimer trace (fsa_trace): {name: (ms per launch, launches per step)}, where a
+        kernel's time is its first block's start to its last block's end, averaged over one
+        replay per (seeds, base_seed) pair (each optionally preceded by ``flush()``).  Unlike
+        event-record nodes, the trace adds no nodes to the graph."""
+        import ctypes as C
+        lib = _lib.load()
+        ns, nb = C.c_int(0), C.c_int(0)
+        _lib.check(lib.fsa_trace_geometry(C.byref(ns), C.byref(nb)), "fsa_trace_geometry")
+        buf = torch.empty((ns.value, nb.value, 2), dtype=torch.int64, device=self.device)
+        tot: dict = {}
+        n = 0
+        try:
+            for seeds, bs in zip(seeds_list, base_seeds):
+                buf[..., 0] = torch.iinfo(torch.int64).max
+                buf[..., 1] = 0
+                _lib.check(lib.fsa_trace(buf.data_ptr()), "fsa_trace")
+                if flush is not None:
+                    flush()
+                self.run(seeds, bs)
+                torch.cuda.synchronize(self.device)
+                _lib.check(lib.fsa_trace(None), "fsa_trace")
+                t = buf.cpu()
+                used = t[..., 1] > 0
+                for slot in range(min(ns.value, len(self.TRACE_NAMES))):
+                    u = used[slot]
+                    if bool(u.any()):
+                        span = float(t[slot, u, 1].max() - t[slot, u, 0].min()) / 1e6
+                        tot[self.TRACE_NAMES[slot]] = tot.get(self.TRACE_NAMES[slot], 0.0) + span
+                n += 1
+        finally:
+            lib.fsa_trace(None)
+        return {k: (v / max(1, n), 1) for k, v in tot.items()}
+
