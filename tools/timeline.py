@@ -76,10 +76,16 @@ def main():
             print(f"phase {ph}: tiles {nt} log2seg {l2} draws {draws} classes " +
                   " ".join(f"[c{c} n{cnt[c]} len{ln[c]} nbn{nbn[c]} t{sgt[c + 1] - sgt[c]}]" for c in nzc[:10]))
         t = buf.cpu().numpy()
+        s2 = ex.s2[1 - ex.parity].reshape(-1)
+        s2 = s2[s2 >= 0]
+        _, cnts = torch.unique(s2, return_counts=True)
+        cn = cnts.cpu().numpy()
+        print(f"slots {s2.numel()} distinct {len(cn)} multi {int((cn > 1).sum())} big(>32) {int((cn > 32).sum())} "
+              f"max count {int(cn.max())} top5 {sorted(cn.tolist())[-5:]}")
         if hasattr(L, "fsa_debug"):
             L.fsa_debug(None)
             d = dbg.view(64, 8).cpu().numpy()
-            tt0 = d[:, 0][d[:, 0] > 0].min()
+            tt0 = t[..., 0][t[..., 1] > 0].min() if False else d[:, 0][d[:, 0] > 0].min()
             for w in range(64):
                 if d[w, 0]:
                     print("warp", w, [(int(x) - tt0) / 1e3 if x > 1e12 else int(x) for x in d[w]])
