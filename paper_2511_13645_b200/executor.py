@@ -153,7 +153,7 @@ class Fused2HopStep:
         return {k: (t / steps / n, n) for k, (t, n) in tot.items()}
 
     TRACE_NAMES = ("k_plan_roots", "k_sample1", "k_plan_hop2", "k_sample2", "k_gather2", "k_zero_rows",
-                   "k_bwd_count", "k_bwd_single", "k_bwd_scatter", "k_bwd_multi")
+                   "k_bwd_count", "k_bwd_single", "k_bwd_scatter", "k_bwd_multi", "k_bwd_big")
 
     def kernel_spans(self, seeds_list, base_seeds, flush=None) -> dict:
         """Per-kernel device time of the normal step graph, from the library's per-block
