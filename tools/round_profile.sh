@@ -1,0 +1,16 @@
+#!/bin/bash
+# Everything the profiles/ directory records for one round: pytest -m gpu, smoke, the default
+# bench line, the timeline trace, an ncu launch list of 3 eager steps and an ncu --set full capture
+# of every kernel of one step.
+mkdir -p gpurun_out
+TAG=${TAG:-r01}
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/${TAG}_smi.txt 2>&1
+timeout 900 python -m pytest tests -m gpu -q > gpurun_out/${TAG}_pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/${TAG}_pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1
+timeout 900 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
+timeout 300 python tools/timeline.py --reps 2 > gpurun_out/${TAG}_timeline.txt 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv \
+    python tools/profile_step.py --alpha 3.0 --steps 3 > /dev/null 2>&1
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_ -s 11 -c 11 \
+    -o gpurun_out/${TAG}_full -f python tools/profile_step.py --alpha 3.0 --steps 3 > gpurun_out/${TAG}_ncu.log 2>&1
+ls gpurun_out | grep ${TAG}
