@@ -127,6 +127,20 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def ncu_traffic(kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one launch of ``kernel`` from the latest
+    committed ncu --set full capture summary (profiles/r*_ncu_traffic.json), or None."""
+    files = sorted((ROOT / "profiles").glob("r*_ncu_traffic.json"))
+    if not files:
+        return None, None
+    try:
+        d = json.loads(files[-1].read_text())
+        k = d["kernels"][kernel]
+        return k["dram_read_bytes"] + k["dram_write_bytes"], files[-1].name
+    except (KeyError, ValueError):
+        return None, files[-1].name
+
+
 def measured_peak_hbm():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -456,8 +470,10 @@ def run_fused(args):
     dom_ms = prof[dom][0]
     kb = kernel_alg_bytes(dom, B, k1, k2, D, E, main["T1"], main["T2"], main["U2"], main["singles"])
     achieved = kb / (dom_ms / 1e3) / 1e9 if kb else None
+    traffic, traffic_src = ncu_traffic(dom)
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": (achieved / peak) if achieved else None, "traffic": None,
+                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "traffic_source": traffic_src, "alg_bytes_per_launch": kb,
                 "peak_kind": peak_kind, "kernel_ms": dom_ms,
                 "share_of_step": prof[dom][0] * prof[dom][1] / main["ms_local"],
                 "timing": "per-block %globaltimer trace of a graph replay after an L2 flush "
