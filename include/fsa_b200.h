@@ -61,6 +61,16 @@ enum fsa_device_error {
 
 enum fsa_op { FSA_OP_FWD1 = 1, FSA_OP_FWD2 = 2, FSA_OP_BWD1 = 3, FSA_OP_BWD2 = 4 };
 
+/* phases of the replay backward (fsa_fused_*_bwd_phase): PLAN needs only the saved ids (per-node
+ * counts, segment reservation, scatter of multi-hit slots), APPLY needs grad_out (the row writes).
+ * PLAN then APPLY on the same workspace == one fsa_fused_*_bwd call. */
+enum fsa_bwd_phase { FSA_BWD_PLAN = 1, FSA_BWD_APPLY = 2, FSA_BWD_ALL = 3 };
+
+/* phases of the 2-hop forward (fsa_fused_2hop_fwd_phase): SAMPLE writes s1/s2/take1/take2 (all
+ * the replay backward's PLAN needs), GATHER the feature means.  SAMPLE then GATHER on the same
+ * workspace == one fsa_fused_2hop_fwd call. */
+enum fsa_fwd_phase { FSA_FWD_SAMPLE = 1, FSA_FWD_GATHER = 2, FSA_FWD_ALL = 3 };
+
 const char* fsa_version(void);
 const char* fsa_status_string(int status);
 int fsa_last_cuda_error(void);
@@ -132,6 +142,16 @@ int fsa_fused_2hop_fwd_dseed(const int32_t* rowptr, const int32_t* col, int64_t 
                              void* out, int64_t out_stride,
                              void* ws, size_t ws_bytes, void* stream);
 
+/* fsa_fused_2hop_fwd in phases (enum fsa_fwd_phase); base_seed_dev, when not NULL, replaces
+ * base_seed by a device-resident value (as the _dseed variant). */
+int fsa_fused_2hop_fwd_phase(const int32_t* rowptr, const int32_t* col, int64_t N,
+                             const void* X, int64_t D, int64_t x_stride, int dtype,
+                             const int64_t* seeds, int64_t B, int64_t root_offset,
+                             int32_t k1, int32_t k2, uint64_t base_seed, const uint64_t* base_seed_dev,
+                             int save, int32_t* s1, int32_t* s2, int32_t* take1, int32_t* take2,
+                             void* out, int64_t out_stride,
+                             void* ws, size_t ws_bytes, void* stream, int phase);
+
 /* ---- backward: deterministic saved-index replay (no float atomics) ----------------------
  * grad_out [B, D] (row stride g_stride) of `dtype`.  For every touched node v the op writes
  *   grad_x[v, :] = (((+0.0 + a_1) + a_2) + ...)   a_i = grad_out[t_i / K] / denom[t_i]
@@ -154,6 +174,22 @@ int fsa_fused_2hop_bwd(const void* grad_out, int64_t B, int64_t D, int64_t g_str
                        void* grad_x, int zero_mode,
                        int32_t* touched, int32_t* n_touched, void* grad_rows,
                        void* ws, size_t ws_bytes, void* stream);
+
+/* The same two ops split into their PLAN / APPLY phases (enum fsa_bwd_phase): a step scheduler
+ * can run PLAN, which reads only the ids, concurrently with the forward's gather or the head that
+ * produces grad_out (grad_out may be NULL for PLAN).  APPLY must follow PLAN on the same
+ * workspace, stream-ordered. */
+int fsa_fused_1hop_bwd_phase(const void* grad_out, int64_t B, int64_t D, int64_t g_stride, int dtype,
+                             const int32_t* samples, const int32_t* takes, int32_t k, int64_t N,
+                             void* grad_x, int zero_mode,
+                             int32_t* touched, int32_t* n_touched, void* grad_rows,
+                             void* ws, size_t ws_bytes, void* stream, int phase);
+
+int fsa_fused_2hop_bwd_phase(const void* grad_out, int64_t B, int64_t D, int64_t g_stride, int dtype,
+                             const int32_t* s1, const int32_t* s2, int32_t k1, int32_t k2, int64_t N,
+                             void* grad_x, int zero_mode,
+                             int32_t* touched, int32_t* n_touched, void* grad_rows,
+                             void* ws, size_t ws_bytes, void* stream, int phase);
 
 /* grad[rows[i], :] = 0 for i < n_rows, rows[i] < 0 skipped (duplicates harmless): sparse
  * re-zero of a persistent gradient buffer between steps, e.g. with the previous step's flat

@@ -14,6 +14,8 @@ from ._build import LIB_PATH
 FSA_OK, FSA_ERR_ARG, FSA_ERR_DTYPE, FSA_ERR_WORKSPACE, FSA_ERR_CUDA, FSA_ERR_ALIGN = range(6)
 FSA_F32, FSA_F64, FSA_BF16, FSA_F16 = range(4)
 FSA_OP_FWD1, FSA_OP_FWD2, FSA_OP_BWD1, FSA_OP_BWD2 = 1, 2, 3, 4
+FSA_BWD_PLAN, FSA_BWD_APPLY, FSA_BWD_ALL = 1, 2, 3
+FSA_FWD_SAMPLE, FSA_FWD_GATHER, FSA_FWD_ALL = 1, 2, 3
 FSA_DEVERR_SEED_RANGE, FSA_DEVERR_INDEX_RANGE, FSA_DEVERR_NEG_TAKE = 1, 2, 4
 
 _p = C.c_void_p
@@ -48,6 +50,12 @@ SIGNATURES = {
                                   _p, _sz, _p]),
     "fsa_fused_2hop_bwd": (_int, [_p, _i64, _i64, _i64, _int, _p, _p, _i32, _i32, _i64, _p, _int, _p,
                                   _p, _p, _p, _sz, _p]),
+    "fsa_fused_2hop_fwd_phase": (_int, [_p, _p, _i64, _p, _i64, _i64, _int, _p, _i64, _i64, _i32, _i32, _u64,
+                                        _p, _int, _p, _p, _p, _p, _p, _i64, _p, _sz, _p, _int]),
+    "fsa_fused_1hop_bwd_phase": (_int, [_p, _i64, _i64, _i64, _int, _p, _p, _i32, _i64, _p, _int, _p, _p, _p,
+                                        _p, _sz, _p, _int]),
+    "fsa_fused_2hop_bwd_phase": (_int, [_p, _i64, _i64, _i64, _int, _p, _p, _i32, _i32, _i64, _p, _int, _p,
+                                        _p, _p, _p, _sz, _p, _int]),
     "fsa_zero_rows": (_int, [_p, _i64, _int, _p, _i64, _p]),
     "fsa_derive_states": (_int, [_p, _p, _p, _p, _i64, _p, _p]),
     "fsa_xorshift_steps": (_int, [_u64, _i64, _p, _p]),

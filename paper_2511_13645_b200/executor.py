@@ -12,7 +12,10 @@ work:
 * the persistent N x D gradient is kept equal to the reference's "zero-filled then scattered"
   buffer by re-zeroing only the rows written in the previous step, on a side stream that runs
   concurrently with the (latency-bound) forward; two graphs alternate s2 buffers so the side
-  stream reads the previous step's ids while the forward writes the current ones.
+  stream reads the previous step's ids while the forward writes the current ones;
+* the replay backward's PLAN phase (per-node counts, segments: it reads only the sampled ids)
+  runs on a second side stream concurrently with the forward's feature gather; only its APPLY
+  phase (the row writes) waits for the gather.
 
 Results are bitwise identical to the eager API (tests/test_gpu_executor.py).
 """
@@ -66,12 +69,16 @@ class Fused2HopStep:
         self.ws_f = torch.zeros(lib.fsa_ws_bytes(_lib.FSA_OP_FWD2, B, k1, k2, 0), dtype=torch.uint8, device=dev)
         self.ws_b = torch.zeros(lib.fsa_ws_bytes(_lib.FSA_OP_BWD2, B, k1, k2, N), dtype=torch.uint8, device=dev)
         self.side = torch.cuda.Stream(device=dev)
+        self.plan = torch.cuda.Stream(device=dev)
         self.parity = 0
         self.graphs = [None, None]
         self.steps_run = 0
 
     # -- raw launch sequence of one step (eager or under capture) ----------------------------
     def _launch(self, parity: int) -> None:
+        """main:   fwd SAMPLE ──┬── fwd GATHER ──┬── bwd APPLY
+           plan:                └── bwd PLAN ────┤        (needs only s1/s2)
+           zero:   re-zero previous rows ────────┘        (sparse, persistent gradient)"""
         lib = _lib.load()
         main = torch.cuda.current_stream(self.device)
         cur, prev = self.s2[parity], self.s2[1 - parity]
@@ -82,18 +89,24 @@ class Fused2HopStep:
             _lib.check(lib.fsa_zero_rows(self.grad.data_ptr(), self.D, self.code, prev.data_ptr(), prev.numel(),
                                          zs.cuda_stream), "fsa_zero_rows")
         st = main.cuda_stream
-        _lib.check(lib.fsa_fused_2hop_fwd_dseed(
-            self.g.rowptr.data_ptr(), self.g.col.data_ptr(), self.N, self.X.data_ptr(), self.D, self.X.stride(0),
-            self.code, self.seeds.data_ptr(), self.B, self.root_offset, self.k1, self.k2,
-            self.base_seed.data_ptr(), 1, self.s1.data_ptr(), cur.data_ptr(), self.t1.data_ptr(),
-            self.t2.data_ptr(), self.out.data_ptr(), self.out.stride(0), self.ws_f.data_ptr(), self.ws_f.numel(),
-            st), "fsa_fused_2hop_fwd_dseed")
+        fwd_args = (self.g.rowptr.data_ptr(), self.g.col.data_ptr(), self.N, self.X.data_ptr(), self.D,
+                    self.X.stride(0), self.code, self.seeds.data_ptr(), self.B, self.root_offset, self.k1, self.k2,
+                    0, self.base_seed.data_ptr(), 1, self.s1.data_ptr(), cur.data_ptr(), self.t1.data_ptr(),
+                    self.t2.data_ptr(), self.out.data_ptr(), self.out.stride(0), self.ws_f.data_ptr(),
+                    self.ws_f.numel(), st)
+        bwd_args = (self.grad_out.data_ptr(), self.B, self.D, self.grad_out.stride(0), self.code,
+                    self.s1.data_ptr(), cur.data_ptr(), self.k1, self.k2, self.N, self.grad.data_ptr(), 0, None,
+                    None, None, self.ws_b.data_ptr(), self.ws_b.numel())
+        _lib.check(lib.fsa_fused_2hop_fwd_phase(*fwd_args, _lib.FSA_FWD_SAMPLE), "fwd SAMPLE")
+        ps = self.plan if self.overlap_zero else main
         if self.overlap_zero:
+            ps.wait_stream(main)
+        _lib.check(lib.fsa_fused_2hop_bwd_phase(*bwd_args, ps.cuda_stream, _lib.FSA_BWD_PLAN), "bwd PLAN")
+        _lib.check(lib.fsa_fused_2hop_fwd_phase(*fwd_args, _lib.FSA_FWD_GATHER), "fwd GATHER")
+        if self.overlap_zero:
+            main.wait_stream(ps)
             main.wait_stream(zs)
-        _lib.check(lib.fsa_fused_2hop_bwd(
-            self.grad_out.data_ptr(), self.B, self.D, self.grad_out.stride(0), self.code, self.s1.data_ptr(),
-            cur.data_ptr(), self.k1, self.k2, self.N, self.grad.data_ptr(), 0, None, None, None,
-            self.ws_b.data_ptr(), self.ws_b.numel(), st), "fsa_fused_2hop_bwd")
+        _lib.check(lib.fsa_fused_2hop_bwd_phase(*bwd_args, st, _lib.FSA_BWD_APPLY), "bwd APPLY")
 
     def _capture(self, parity: int) -> torch.cuda.CUDAGraph:
         # warm the launch path once outside capture (device init, function attributes)
@@ -153,7 +166,8 @@ class Fused2HopStep:
         return {k: (t / steps / n, n) for k, (t, n) in tot.items()}
 
     TRACE_NAMES = ("k_plan_roots", "k_sample1", "k_plan_hop2", "k_sample2", "k_gather2", "k_zero_rows",
-                   "k_bwd_count", "k_bwd_single", "k_bwd_scatter", "k_bwd_multi", "k_bwd_big")
+                   "k_bwd_count", "k_bwd_single", "k_bwd_scatter", "k_bwd_multi", "k_bwd_big", "k_bwd_reserve",
+                   "k_final2")
 
     def kernel_spans(self, seeds_list, base_seeds, flush=None) -> dict:
         """Per-kernel device time of the normal step graph, from the library's per-block

@@ -19,7 +19,7 @@ from paper_2511_13645_b200 import _lib, synth  # noqa: E402
 from paper_2511_13645_b200.executor import Fused2HopStep  # noqa: E402
 
 NAMES = ["plan_roots", "sample1", "plan_hop2", "sample2", "gather", "zero_rows", "bwd_count", "bwd_single",
-         "bwd_scatter", "bwd_multi", "bwd_big"]
+         "bwd_scatter", "bwd_multi", "bwd_big", "bwd_reserve", "final2"]
 
 
 def main():
@@ -65,16 +65,6 @@ def main():
         ev[1].record()
         torch.cuda.synchronize()
         _lib.check(_lib.load().fsa_trace(None), "trace off")
-        hdr = ex.ws_f[:8192].cpu().numpy()
-        for ph in range(2):
-            o = 256 + ph * 2592
-            ints = hdr[o:o + 2592].view(np.int32)
-            nt, done, ctr, l2 = ints[:4]
-            draws = int(hdr[o + 16:o + 24].view(np.int64)[0])
-            cnt, ln, cst, nbn, sgt = ints[6:134], ints[134:262], ints[262:391], ints[391:519], ints[519:648]
-            nzc = np.flatnonzero(cnt)
-            print(f"phase {ph}: tiles {nt} log2seg {l2} draws {draws} classes " +
-                  " ".join(f"[c{c} n{cnt[c]} len{ln[c]} nbn{nbn[c]} t{sgt[c + 1] - sgt[c]}]" for c in nzc[:10]))
         t = buf.cpu().numpy()
         s2 = ex.s2[1 - ex.parity].reshape(-1)
         s2 = s2[s2 >= 0]
