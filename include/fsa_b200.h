@@ -206,6 +206,9 @@ int fsa_jump(const uint64_t* states, const int64_t* dist, int64_t n, uint64_t* o
  * division differs bitwise from IEEE division: every divisor 1..dmax against every fp32
  * significand of two binades, plus sampled fp64 inputs. */
 int fsa_div_check(int dmax, unsigned long long* mismatches, void* stream);
+/* Micro-benchmark of the sampler's draw loop: one warp of `lanes` lanes, n draws per lane from
+ * modulus m0 (mode 0 Barrett, 1 fraction test); out[0] = clock64 cycles, out[1] checksum. */
+int fsa_bench_draws(int mode, int n, uint32_t m0, int k, int lanes, unsigned long long* out, void* stream);
 /* out[i] = x[i] % m[i] through the Barrett path used by the sampler (2 <= m <= 2^30) */
 int fsa_umod(const uint64_t* x, const uint32_t* m, int64_t n, uint32_t* out, void* stream);
 

@@ -62,6 +62,7 @@ SIGNATURES = {
     "fsa_jump": (_int, [_p, _p, _i64, _p, _p]),
     "fsa_umod": (_int, [_p, _p, _i64, _p, _p]),
     "fsa_div_check": (_int, [_int, _p, _p]),
+    "fsa_bench_draws": (_int, [_int, _int, C.c_uint32, _int, _int, _p, _p]),
 }
 
 _LIB = None
