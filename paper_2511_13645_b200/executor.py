@@ -57,10 +57,15 @@ class Fused2HopStep:
         lib = _lib.load()
         _set_device(dev)
         B, k1, k2, D, N = self.B, self.k1, self.k2, self.D, self.N
-        self.seeds = torch.zeros(B, dtype=torch.int64, device=dev)
-        self.base_seed = torch.zeros(1, dtype=torch.int64, device=dev)
-        self.grad_out = torch.zeros((B, D), dtype=self.dtype, device=dev)
-        self.out = torch.empty((B, D), dtype=self.dtype, device=dev)
+        # per-parity inputs / output: step i+1's host->device copies overlap step i's compute
+        self.seeds_p = [torch.zeros(B, dtype=torch.int64, device=dev) for _ in range(2)]
+        self.base_seed_p = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(2)]
+        self.grad_out_p = [torch.zeros((B, D), dtype=self.dtype, device=dev) for _ in range(2)]
+        self.out_p = [torch.empty((B, D), dtype=self.dtype, device=dev) for _ in range(2)]
+        self.copy = torch.cuda.Stream(device=dev)      # host -> device inputs
+        self.copy_out = torch.cuda.Stream(device=dev)  # device -> host outputs
+        self.done = [torch.cuda.Event() for _ in range(2)]
+        self.done_used = [False, False]
         self.s1 = torch.empty((B, k1), dtype=torch.int32, device=dev)
         self.s2 = [torch.full((B, k1, k2), -1, dtype=torch.int32, device=dev) for _ in range(2)]
         self.t1 = torch.empty(B, dtype=torch.int32, device=dev)
@@ -82,6 +87,8 @@ class Fused2HopStep:
         lib = _lib.load()
         main = torch.cuda.current_stream(self.device)
         cur, prev = self.s2[parity], self.s2[1 - parity]
+        seeds, base_seed = self.seeds_p[parity], self.base_seed_p[parity]
+        grad_out, out = self.grad_out_p[parity], self.out_p[parity]
         zs = self.side if self.overlap_zero else main
         if self.overlap_zero:
             zs.wait_stream(main)
@@ -90,11 +97,11 @@ class Fused2HopStep:
                                          zs.cuda_stream), "fsa_zero_rows")
         st = main.cuda_stream
         fwd_args = (self.g.rowptr.data_ptr(), self.g.col.data_ptr(), self.N, self.X.data_ptr(), self.D,
-                    self.X.stride(0), self.code, self.seeds.data_ptr(), self.B, self.root_offset, self.k1, self.k2,
-                    0, self.base_seed.data_ptr(), 1, self.s1.data_ptr(), cur.data_ptr(), self.t1.data_ptr(),
-                    self.t2.data_ptr(), self.out.data_ptr(), self.out.stride(0), self.ws_f.data_ptr(),
+                    self.X.stride(0), self.code, seeds.data_ptr(), self.B, self.root_offset, self.k1, self.k2,
+                    0, base_seed.data_ptr(), 1, self.s1.data_ptr(), cur.data_ptr(), self.t1.data_ptr(),
+                    self.t2.data_ptr(), out.data_ptr(), out.stride(0), self.ws_f.data_ptr(),
                     self.ws_f.numel(), st)
-        bwd_args = (self.grad_out.data_ptr(), self.B, self.D, self.grad_out.stride(0), self.code,
+        bwd_args = (grad_out.data_ptr(), self.B, self.D, grad_out.stride(0), self.code,
                     self.s1.data_ptr(), cur.data_ptr(), self.k1, self.k2, self.N, self.grad.data_ptr(), 0, None,
                     None, None, self.ws_b.data_ptr(), self.ws_b.numel())
         _lib.check(lib.fsa_fused_2hop_fwd_phase(*fwd_args, _lib.FSA_FWD_SAMPLE), "fwd SAMPLE")
@@ -115,17 +122,44 @@ class Fused2HopStep:
             self._launch(parity)
         return g
 
-    def run(self, seeds: Optional[torch.Tensor], base_seed: int, grad_out: Optional[torch.Tensor] = None):
-        """One step.  ``seeds`` (int64 [B], device or pinned host) and ``grad_out`` ([B, D]) are
-        copied into the static buffers (pass None to reuse what is there).  Returns
-        ``(out, SampledIndices2)`` views of the static buffers, valid until the next call."""
-        if seeds is not None:
-            self.seeds.copy_(seeds, non_blocking=True)
-        b = int(base_seed) & 0xFFFFFFFFFFFFFFFF
-        self.base_seed.fill_(b - (1 << 64) if b >= (1 << 63) else b)  # same 64 bits, int64 storage
-        if grad_out is not None:
-            self.grad_out.copy_(grad_out, non_blocking=True)
+    @property
+    def out(self) -> torch.Tensor:
+        """Output of the most recent step."""
+        return self.out_p[1 - self.parity]
+
+    def set_grad_out(self, grad_out: torch.Tensor) -> None:
+        """Fill both grad_out buffers (steps run with ``grad_out=None`` then reuse it)."""
+        for g in self.grad_out_p:
+            g.copy_(grad_out)
+
+    def run(self, seeds: Optional[torch.Tensor], base_seed: int, grad_out: Optional[torch.Tensor] = None,
+            out_host: Optional[torch.Tensor] = None):
+        """One step.  ``seeds`` (int64 [B]) and ``grad_out`` ([B, D]) may be device tensors or
+        pinned host tensors; host inputs are copied on a copy stream into this step's buffers
+        (two sets, alternating), so the copies overlap the previous step's compute.  Pass
+        ``grad_out=None`` to reuse what the buffer holds.  With ``out_host`` (pinned, [B, D]) the
+        step's output is copied back on the copy stream after the step.  ``grad_out=None`` reuses
+        the content of this parity's buffer (see set_grad_out).  Returns
+        ``(out, SampledIndices2)`` views of static buffers, valid until the step after next."""
         p = self.parity
+        main = torch.cuda.current_stream(self.device)
+        host_in = (seeds is not None and not seeds.is_cuda) or (grad_out is not None and not grad_out.is_cuda)
+        if host_in:
+            if self.done_used[p]:
+                self.copy.wait_event(self.done[p])  # the step that last read these buffers is done
+            with torch.cuda.stream(self.copy):
+                if seeds is not None:
+                    self.seeds_p[p].copy_(seeds, non_blocking=True)
+                if grad_out is not None:
+                    self.grad_out_p[p].copy_(grad_out, non_blocking=True)
+            main.wait_stream(self.copy)
+        else:
+            if seeds is not None:
+                self.seeds_p[p].copy_(seeds, non_blocking=True)
+            if grad_out is not None:
+                self.grad_out_p[p].copy_(grad_out, non_blocking=True)
+        b = int(base_seed) & 0xFFFFFFFFFFFFFFFF
+        self.base_seed_p[p].fill_(b - (1 << 64) if b >= (1 << 63) else b)  # same 64 bits, int64 storage
         if self.use_graph:
             if self.steps_run < 2:  # first use of each parity runs eagerly (init, attributes)
                 self._launch(p)
@@ -135,9 +169,21 @@ class Fused2HopStep:
                 self.graphs[p].replay()
         else:
             self._launch(p)
+        self.done[p].record(main)
+        self.done_used[p] = True
+        if out_host is not None:  # on its own stream: the next step's input copies do not queue behind it
+            self.copy_out.wait_event(self.done[p])
+            with torch.cuda.stream(self.copy_out):
+                out_host.copy_(self.out_p[p], non_blocking=True)
         self.steps_run += 1
         self.parity = 1 - p
-        return self.out, SampledIndices2(self.s1, self.s2[p])
+        return self.out_p[p], SampledIndices2(self.s1, self.s2[p])
+
+    def sync_copies(self) -> None:
+        """Make the current stream wait for the copy streams (pending D2H of outputs)."""
+        cur = torch.cuda.current_stream(self.device)
+        cur.wait_stream(self.copy)
+        cur.wait_stream(self.copy_out)
 
     def kernel_times(self, seeds_list, base_seeds, flush=None) -> dict:
         """Per-kernel device time inside the captured step graph: {name: (ms per launch, launches
@@ -149,9 +195,9 @@ class Fused2HopStep:
             g = self._capture(self.parity)
             tot: dict = {}
             for seeds, bs in zip(seeds_list, base_seeds):
-                self.seeds.copy_(seeds, non_blocking=True)
+                self.seeds_p[self.parity].copy_(seeds, non_blocking=True)
                 b = int(bs) & 0xFFFFFFFFFFFFFFFF
-                self.base_seed.fill_(b - (1 << 64) if b >= (1 << 63) else b)
+                self.base_seed_p[self.parity].fill_(b - (1 << 64) if b >= (1 << 63) else b)
                 if flush is not None:
                     flush()
                 g.replay()

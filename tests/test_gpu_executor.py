@@ -1,6 +1,7 @@
 """The CUDA-graph step executor is bitwise identical to the eager operator API, step after
 step (fresh neighbourhoods per base seed, persistent gradient buffer kept equal to the
-reference's zero-filled-then-scattered buffer)."""
+reference's zero-filled-then-scattered buffer), with device inputs and with pinned host inputs
+copied on its copy stream (outputs copied back the same way)."""
 
 import numpy as np
 import pytest
@@ -11,8 +12,9 @@ from conftest import iter_cases
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("use_graph,overlap", [(True, True), (False, False), (True, False)])
-def test_executor_matches_eager(golden_powerlaw, use_graph, overlap):
+@pytest.mark.parametrize("use_graph,overlap,host", [(True, True, False), (False, False, False), (True, False, False),
+                                                    (True, True, True)])
+def test_executor_matches_eager(golden_powerlaw, use_graph, overlap, host):
     import paper_2511_13645_b200 as fsa
     from paper_2511_13645_b200.executor import Fused2HopStep
 
@@ -22,14 +24,21 @@ def test_executor_matches_eager(golden_powerlaw, use_graph, overlap):
         B = 64
         ex = Fused2HopStep(g, X, B, c["k1"], c["k2"], root_offset=5, use_graph=use_graph, overlap_zero=overlap)
         rng = np.random.default_rng(3)
+        h_out = [torch.empty((B, X.shape[1]), dtype=X.dtype).pin_memory() for _ in range(2)]
         for step in range(6):
-            seeds = torch.as_tensor(rng.integers(0, c["N"], size=B)).cuda()
-            gout = torch.randn((B, X.shape[1]), device="cuda")
+            seeds = torch.as_tensor(rng.integers(0, c["N"], size=B))
+            gout = torch.randn((B, X.shape[1]))
             bs = fsa.step_seed(42, step)
-            out, idx = ex.run(seeds, bs, gout)
-            ref_out, ref_idx = fsa.fused_2hop_forward(g, X, seeds, c["k1"], c["k2"], bs, root_offset=5)
-            ref_grad = fsa.fused_2hop_backward(gout, ref_idx, c["N"])
+            if host:
+                out, idx = ex.run(seeds.pin_memory(), bs, gout.pin_memory(), out_host=h_out[step % 2])
+                ex.sync_copies()
+            else:
+                out, idx = ex.run(seeds.cuda(), bs, gout.cuda())
+            ref_out, ref_idx = fsa.fused_2hop_forward(g, X, seeds.cuda(), c["k1"], c["k2"], bs, root_offset=5)
+            ref_grad = fsa.fused_2hop_backward(gout.cuda(), ref_idx, c["N"])
             torch.cuda.synchronize()
             assert torch.equal(out, ref_out), (name, step)
+            if host:
+                assert torch.equal(h_out[step % 2], ref_out.cpu()), (name, step)
             assert torch.equal(idx.s1, ref_idx.s1) and torch.equal(idx.s2, ref_idx.s2), (name, step)
             assert torch.equal(ex.grad, ref_grad), (name, step)
