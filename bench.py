@@ -383,7 +383,8 @@ def max_over_ranks(x, world, device):
     if world == 1:
         return x
     import torch
-    t = torch.tensor([x], dtype=torch.float64, device=device)
+    on_dev = torch.distributed.get_backend() == "nccl"
+    t = torch.tensor([x], dtype=torch.float64, device=device if on_dev else "cpu")
     torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     return float(t.item())
 
@@ -433,16 +434,24 @@ def run_fused(args):
     from paper_2511_13645_b200 import synth
 
     world, rank, local = dist_env()
+    # one process per GPU over NCCL; FSA_DIST_BACKEND=gloo lets a 1-GPU box exercise the
+    # multi-rank path (ranks then share cuda:0, which NCCL refuses) - a functional check only
+    backend = os.environ.get("FSA_DIST_BACKEND", "nccl")
+    ndev = torch.cuda.device_count()
+    gpu = local % max(1, ndev) if backend != "nccl" else local
     if world > 1:
-        torch.cuda.set_device(local)
-        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
-    device = torch.device("cuda", local)
+        torch.cuda.set_device(gpu)
+        if backend == "nccl":
+            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", gpu))
+        else:
+            torch.distributed.init_process_group(backend)
+    device = torch.device("cuda", gpu)
     torch.cuda.set_device(device)
     shape = synth.SHAPES[args.config]
 
     def measure(alpha, full=True):
         r = Runner(args, shape, alpha, device, world, rank)
-        with ClockSampler(local) as clk:
+        with ClockSampler(gpu) as clk:
             ms, launches, wall = r.timed(args.steps, args.warmup)
         mean_ms = statistics.mean(ms)
         ms_max = max_over_ranks(mean_ms, world, device)
