@@ -431,6 +431,11 @@ def cpu_model():
 # ----------------------------------------------------------------------------------------------
 def run_fused(args):
     import torch
+    if os.environ.get("FSA_SEG_DIV"):  # experiment knob: sampler bucket-length divisor
+        from paper_2511_13645_b200 import _lib
+        lib = _lib.load()
+        lib.fsa_tune.argtypes = [_lib.C.c_int, _lib.C.c_int]
+        lib.fsa_tune(1, int(os.environ["FSA_SEG_DIV"]))
     from paper_2511_13645_b200 import synth
 
     world, rank, local = dist_env()
