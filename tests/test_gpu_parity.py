@@ -368,3 +368,40 @@ def test_division_hook(fsa):
     _lib.check(_lib.load().fsa_div_check(4096, bad.data_ptr(), torch.cuda.current_stream().cuda_stream), "div")
     torch.cuda.synchronize()
     assert int(bad.item()) == 0
+
+
+def test_phase_entry_points_equal_monolithic_calls(fsa, golden_powerlaw):
+    """fsa_fused_2hop_fwd_phase (SAMPLE, GATHER) and fsa_fused_2hop_bwd_phase (PLAN, APPLY), the
+    split the step executor schedules across streams, give the monolithic calls' results bitwise."""
+    from paper_2511_13645_b200 import _lib
+    lib = _lib.load()
+    name, c = next(iter_cases(golden_powerlaw))
+    g = dev_graph(fsa, c["rowptr"], c["col"], c["N"])
+    X, seeds = T(c["X"]), T(c["seeds"])
+    B, k1, k2, D, N = seeds.numel(), c["k1"], c["k2"], X.shape[1], c["N"]
+    ref_out, ref_idx = fsa.fused_2hop_forward(g, X, seeds, k1, k2, c["base_seed"])
+    gout = torch.randn((B, D), device="cuda", dtype=X.dtype)
+    ref_grad = fsa.fused_2hop_backward(gout, ref_idx, N)
+    st = torch.cuda.current_stream().cuda_stream
+    ws_f = torch.zeros(lib.fsa_ws_bytes(_lib.FSA_OP_FWD2, B, k1, k2, 0), dtype=torch.uint8, device="cuda")
+    ws_b = torch.zeros(lib.fsa_ws_bytes(_lib.FSA_OP_BWD2, B, k1, k2, N), dtype=torch.uint8, device="cuda")
+    out = torch.empty_like(ref_out)
+    s1 = torch.empty((B, k1), dtype=torch.int32, device="cuda")
+    s2 = torch.empty((B, k1, k2), dtype=torch.int32, device="cuda")
+    t1 = torch.empty(B, dtype=torch.int32, device="cuda")
+    t2 = torch.empty((B, k1), dtype=torch.int32, device="cuda")
+    code = _lib.FSA_F32 if X.dtype == torch.float32 else _lib.FSA_F64
+    for phase in (_lib.FSA_FWD_SAMPLE, _lib.FSA_FWD_GATHER):
+        _lib.check(lib.fsa_fused_2hop_fwd_phase(
+            g.rowptr.data_ptr(), g.col.data_ptr(), N, X.data_ptr(), D, X.stride(0), code, seeds.data_ptr(), B, 0,
+            k1, k2, c["base_seed"] & (2**64 - 1), None, 1, s1.data_ptr(), s2.data_ptr(), t1.data_ptr(),
+            t2.data_ptr(), out.data_ptr(), out.stride(0), ws_f.data_ptr(), ws_f.numel(), st, phase), "fwd phase")
+    grad = torch.zeros((N, D), device="cuda", dtype=X.dtype)
+    for phase in (_lib.FSA_BWD_PLAN, _lib.FSA_BWD_APPLY):
+        _lib.check(lib.fsa_fused_2hop_bwd_phase(
+            gout.data_ptr(), B, D, D, code, s1.data_ptr(), s2.data_ptr(), k1, k2, N, grad.data_ptr(), 0, None, None,
+            None, ws_b.data_ptr(), ws_b.numel(), st, phase), "bwd phase")
+    torch.cuda.synchronize()
+    assert torch.equal(s1, ref_idx.s1) and torch.equal(s2, ref_idx.s2)
+    assert torch.equal(out, ref_out)
+    assert torch.equal(grad, ref_grad)
