@@ -405,3 +405,30 @@ def test_phase_entry_points_equal_monolithic_calls(fsa, golden_powerlaw):
     assert torch.equal(s1, ref_idx.s1) and torch.equal(s2, ref_idx.s2)
     assert torch.equal(out, ref_out)
     assert torch.equal(grad, ref_grad)
+
+
+@pytest.mark.parametrize("B,leaves", [(40, 64), (1024, 3000)])
+def test_hub_hit_by_every_slot(fsa, oracle_mod, B, leaves):
+    """A star graph whose roots are all the centre: every second-hop slot samples the centre, so
+    the replay backward sums B * k1 terms into one row (k_bwd_big: counting sort at 600 hits,
+    bitmap windows at 15 360) — bitwise against the oracle."""
+    n = leaves + 1
+    rowptr = np.zeros(n + 1, np.int64)
+    rowptr[1] = leaves
+    rowptr[2:] = leaves + np.arange(1, leaves + 1)
+    col = np.concatenate([np.arange(1, n), np.zeros(leaves, np.int64)]).astype(np.int32)
+    g = dev_graph(fsa, rowptr, col, n)
+    rng = np.random.default_rng(11)
+    X = rng.standard_normal((n, 40)).astype(np.float32)
+    seeds = np.zeros(B, np.int64)
+    k1, k2, bs = 15, 10, 1234567
+    out, idx = fsa.fused_2hop_forward(g, T(X), T(seeds), k1, k2, bs)
+    gout = rng.standard_normal((B, 40)).astype(np.float32)
+    grad = fsa.fused_2hop_backward(T(gout), idx, n)
+    torch.cuda.synchronize()
+    ref_out, s1, s2, _, _ = oracle_mod.fused_2hop(rowptr.astype(np.int32), col, X, seeds, k1, k2, bs)
+    ref_grad = oracle_mod.backward_2hop(gout, s1, s2, n)
+    assert int((s2 == 0).sum()) == B * k1
+    assert np.array_equal(idx.s2.cpu().numpy(), s2)
+    assert bitwise(out, ref_out)
+    assert bitwise(grad, ref_grad)
