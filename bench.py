@@ -184,6 +184,8 @@ def kernel_alg_bytes(name, B, k1, k2, D, E, T1, T2, U2, singles):
         return E * D * singles + 4 * B * k1 * k2 + 4 * U2
     if name == "k_bwd_multi":
         return E * D * (U2 - singles) + 4 * (T2 - singles)
+    if name == "k_bwd_terms":  # grad_out rows + the fp32 term table (G = B*k1 rows) + denominators
+        return E * D * B + 4 * D * B * k1 + 4 * B * k1
     if name == "k_zero_rows":
         return E * D * T2 + 4 * B * k1 * k2
     return None

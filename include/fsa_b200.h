@@ -62,9 +62,18 @@ enum fsa_device_error {
 enum fsa_op { FSA_OP_FWD1 = 1, FSA_OP_FWD2 = 2, FSA_OP_BWD1 = 3, FSA_OP_BWD2 = 4 };
 
 /* phases of the replay backward (fsa_fused_*_bwd_phase): PLAN needs only the saved ids (per-node
- * counts, segment reservation, scatter of multi-hit slots), APPLY needs grad_out (the row writes).
- * PLAN then APPLY on the same workspace == one fsa_fused_*_bwd call. */
-enum fsa_bwd_phase { FSA_BWD_PLAN = 1, FSA_BWD_APPLY = 2, FSA_BWD_ALL = 3 };
+ * counts, segment reservation, scatter of multi-hit slots); TERMS needs grad_out and the saved
+ * ids, not PLAN (the per-group quotient table grad_out[row] / den in the workspace), so the two
+ * may run concurrently on different streams; ROWS needs both (the gradient row writes; grad_out
+ * is not read).  PLAN and TERMS (either order or concurrent), then ROWS, on the same workspace
+ * == one fsa_fused_*_bwd call. */
+enum fsa_bwd_phase {
+  FSA_BWD_PLAN = 1,
+  FSA_BWD_TERMS = 2,
+  FSA_BWD_ROWS = 4,
+  FSA_BWD_APPLY = 6, /* TERMS | ROWS */
+  FSA_BWD_ALL = 7
+};
 
 /* phases of the 2-hop forward (fsa_fused_2hop_fwd_phase): SAMPLE writes s1/s2/take1/take2 (all
  * the replay backward's PLAN needs), GATHER the feature means.  SAMPLE then GATHER on the same
@@ -94,9 +103,11 @@ int fsa_profile_read(int max_kernels, char* names, double* total_ms, int64_t* la
 int fsa_trace(void* buf);
 int fsa_trace_geometry(int* slots, int* blocks);
 
-/* Workspace bytes for `op`.  FWD1: (B, k1=k); FWD2: (B, k1, k2); BWD1: (B, k1=k, N);
- * BWD2: (B, k1, k2, N).  Unused arguments are ignored. */
-size_t fsa_ws_bytes(int op, int64_t B, int32_t k1, int32_t k2, int64_t N);
+/* Workspace bytes for `op`.  FWD1: (B, k1=k); FWD2: (B, k1, k2); BWD1: (B, k1=k, D, dtype, N);
+ * BWD2: (B, k1, k2, D, dtype, N) -- a backward workspace holds the term table, G x D values in
+ * the accumulation type (fp64 for FSA_F64, else fp32).  Unused arguments are ignored; 0 means
+ * an invalid request. */
+size_t fsa_ws_bytes(int op, int64_t B, int32_t k1, int32_t k2, int64_t D, int dtype, int64_t N);
 
 /* Synchronously read (and optionally clear) the device error word of a workspace. */
 int fsa_read_error(void* ws, int clear, int* flags, void* stream);
@@ -175,10 +186,10 @@ int fsa_fused_2hop_bwd(const void* grad_out, int64_t B, int64_t D, int64_t g_str
                        int32_t* touched, int32_t* n_touched, void* grad_rows,
                        void* ws, size_t ws_bytes, void* stream);
 
-/* The same two ops split into their PLAN / APPLY phases (enum fsa_bwd_phase): a step scheduler
- * can run PLAN, which reads only the ids, concurrently with the forward's gather or the head that
- * produces grad_out (grad_out may be NULL for PLAN).  APPLY must follow PLAN on the same
- * workspace, stream-ordered. */
+/* The same two ops split into phases (enum fsa_bwd_phase): a step scheduler can run PLAN, which
+ * reads only the ids, concurrently with the forward's gather or the head that produces grad_out
+ * (grad_out may be NULL unless the TERMS bit is set), and TERMS as soon as grad_out exists.
+ * Phases must follow each other on the same workspace, stream-ordered. */
 int fsa_fused_1hop_bwd_phase(const void* grad_out, int64_t B, int64_t D, int64_t g_stride, int dtype,
                              const int32_t* samples, const int32_t* takes, int32_t k, int64_t N,
                              void* grad_x, int zero_mode,

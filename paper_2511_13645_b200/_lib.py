@@ -14,7 +14,7 @@ from ._build import LIB_PATH
 FSA_OK, FSA_ERR_ARG, FSA_ERR_DTYPE, FSA_ERR_WORKSPACE, FSA_ERR_CUDA, FSA_ERR_ALIGN = range(6)
 FSA_F32, FSA_F64, FSA_BF16, FSA_F16 = range(4)
 FSA_OP_FWD1, FSA_OP_FWD2, FSA_OP_BWD1, FSA_OP_BWD2 = 1, 2, 3, 4
-FSA_BWD_PLAN, FSA_BWD_APPLY, FSA_BWD_ALL = 1, 2, 3
+FSA_BWD_PLAN, FSA_BWD_TERMS, FSA_BWD_ROWS, FSA_BWD_APPLY, FSA_BWD_ALL = 1, 2, 4, 6, 7
 FSA_FWD_SAMPLE, FSA_FWD_GATHER, FSA_FWD_ALL = 1, 2, 3
 FSA_DEVERR_SEED_RANGE, FSA_DEVERR_INDEX_RANGE, FSA_DEVERR_NEG_TAKE = 1, 2, 4
 
@@ -36,7 +36,7 @@ SIGNATURES = {
     "fsa_profile_read": (_int, [_int, _p, _p, _p, C.POINTER(_int)]),
     "fsa_trace": (_int, [_p]),
     "fsa_trace_geometry": (_int, [C.POINTER(_int), C.POINTER(_int)]),
-    "fsa_ws_bytes": (_sz, [_int, _i64, _i32, _i32, _i64]),
+    "fsa_ws_bytes": (_sz, [_int, _i64, _i32, _i32, _i64, _int, _i64]),
     "fsa_read_error": (_int, [_p, _int, C.POINTER(_int), _p]),
     "fsa_fused_1hop_fwd": (_int, [_p, _p, _i64, _p, _i64, _i64, _int, _p, _i64, _i64, _i32, _u64, _int,
                                   _p, _p, _p, _i64, _p, _sz, _p]),

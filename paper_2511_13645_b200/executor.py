@@ -22,6 +22,8 @@ Results are bitwise identical to the eager API (tests/test_gpu_executor.py).
 
 from __future__ import annotations
 
+import os
+
 from typing import Optional
 
 import torch
@@ -71,19 +73,20 @@ class Fused2HopStep:
         self.t1 = torch.empty(B, dtype=torch.int32, device=dev)
         self.t2 = torch.empty((B, k1), dtype=torch.int32, device=dev)
         self.grad = torch.zeros((N, D), dtype=self.dtype, device=dev)
-        self.ws_f = torch.zeros(lib.fsa_ws_bytes(_lib.FSA_OP_FWD2, B, k1, k2, 0), dtype=torch.uint8, device=dev)
-        self.ws_b = torch.zeros(lib.fsa_ws_bytes(_lib.FSA_OP_BWD2, B, k1, k2, N), dtype=torch.uint8, device=dev)
+        self.ws_f = torch.zeros(lib.fsa_ws_bytes(_lib.FSA_OP_FWD2, B, k1, k2, 0, 0, 0), dtype=torch.uint8, device=dev)
+        self.ws_b = torch.zeros(lib.fsa_ws_bytes(_lib.FSA_OP_BWD2, B, k1, k2, D, self.code, N), dtype=torch.uint8, device=dev)
         self.side = torch.cuda.Stream(device=dev)
-        self.plan = torch.cuda.Stream(device=dev)
+        # the backward branch (PLAN -> ROWS) shares the SMs with the gather; it is the longer branch
+        self.plan = torch.cuda.Stream(device=dev, priority=int(os.environ.get("FSA_PLAN_PRIO", "0")))
         self.parity = 0
         self.graphs = [None, None]
         self.steps_run = 0
 
     # -- raw launch sequence of one step (eager or under capture) ----------------------------
     def _launch(self, parity: int) -> None:
-        """main:   fwd SAMPLE ──┬── fwd GATHER ──┬── bwd APPLY
-           plan:                └── bwd PLAN ────┤        (needs only s1/s2)
-           zero:   re-zero previous rows ────────┘        (sparse, persistent gradient)"""
+        """main:   fwd SAMPLE ──┬── fwd GATHER ─────────────────────┬── (step end)
+           plan:                ├── bwd PLAN ──────┬── bwd ROWS ──┘  (PLAN needs only s1/s2)
+           zero:   re-zero prev rows ── bwd TERMS ─┘                 (grad_out + s1/s2)"""
         lib = _lib.load()
         main = torch.cuda.current_stream(self.device)
         cur, prev = self.s2[parity], self.s2[1 - parity]
@@ -105,15 +108,22 @@ class Fused2HopStep:
                     self.s1.data_ptr(), cur.data_ptr(), self.k1, self.k2, self.N, self.grad.data_ptr(), 0, None,
                     None, None, self.ws_b.data_ptr(), self.ws_b.numel())
         _lib.check(lib.fsa_fused_2hop_fwd_phase(*fwd_args, _lib.FSA_FWD_SAMPLE), "fwd SAMPLE")
-        ps = self.plan if self.overlap_zero else main
-        if self.overlap_zero:
-            ps.wait_stream(main)
+        if not self.overlap_zero:
+            for ph in (_lib.FSA_BWD_PLAN, _lib.FSA_BWD_TERMS):
+                _lib.check(lib.fsa_fused_2hop_bwd_phase(*bwd_args, st, ph), "bwd phase")
+            _lib.check(lib.fsa_fused_2hop_fwd_phase(*fwd_args, _lib.FSA_FWD_GATHER), "fwd GATHER")
+            _lib.check(lib.fsa_fused_2hop_bwd_phase(*bwd_args, st, _lib.FSA_BWD_ROWS), "bwd ROWS")
+            return
+        # the backward does not read the gather's output: PLAN -> ROWS run as one branch beside it
+        ps = self.plan
+        ps.wait_stream(main)
+        zs.wait_stream(main)  # TERMS after the re-zeroing, on the same side stream
+        _lib.check(lib.fsa_fused_2hop_bwd_phase(*bwd_args, zs.cuda_stream, _lib.FSA_BWD_TERMS), "bwd TERMS")
         _lib.check(lib.fsa_fused_2hop_bwd_phase(*bwd_args, ps.cuda_stream, _lib.FSA_BWD_PLAN), "bwd PLAN")
         _lib.check(lib.fsa_fused_2hop_fwd_phase(*fwd_args, _lib.FSA_FWD_GATHER), "fwd GATHER")
-        if self.overlap_zero:
-            main.wait_stream(ps)
-            main.wait_stream(zs)
-        _lib.check(lib.fsa_fused_2hop_bwd_phase(*bwd_args, st, _lib.FSA_BWD_APPLY), "bwd APPLY")
+        ps.wait_stream(zs)  # term table written, previous rows zeroed
+        _lib.check(lib.fsa_fused_2hop_bwd_phase(*bwd_args, ps.cuda_stream, _lib.FSA_BWD_ROWS), "bwd ROWS")
+        main.wait_stream(ps)
 
     def _capture(self, parity: int) -> torch.cuda.CUDAGraph:
         # warm the launch path once outside capture (device init, function attributes)
@@ -213,7 +223,7 @@ class Fused2HopStep:
 
     TRACE_NAMES = ("k_plan_roots", "k_sample1", "k_plan_hop2", "k_sample2", "k_gather2", "k_zero_rows",
                    "k_bwd_count", "k_bwd_single", "k_bwd_scatter", "k_bwd_multi", "k_bwd_big", "k_bwd_reserve",
-                   "k_final2")
+                   "k_final2", "k_bwd_terms")
 
     def kernel_spans(self, seeds_list, base_seeds, flush=None) -> dict:
         """Per-kernel device time of the normal step graph, from the library's per-block

@@ -99,9 +99,10 @@ class SampledIndices2:
 _tls = threading.local()
 
 
-def _ws(op: int, B: int, k1: int, k2: int, N: int, device: torch.device, stream: int) -> torch.Tensor:
+def _ws(op: int, B: int, k1: int, k2: int, N: int, device: torch.device, stream: int, D: int = 0,
+        dtype_code: int = 0) -> torch.Tensor:
     """Cached, zero-initialised workspace per (device, stream, op kind)."""
-    need = _lib.load().fsa_ws_bytes(op, B, k1, k2, N)
+    need = _lib.load().fsa_ws_bytes(op, B, k1, k2, D, dtype_code, N)
     if need == 0:
         raise ValueError("invalid workspace request")
     cache = getattr(_tls, "ws", None)
@@ -414,7 +415,7 @@ def fused_1hop_backward(grad_out, indices: Optional[SampledIndices1], num_nodes:
     buf, mode = _grad_buffer(g, num_nodes, None if host_mode else out, zero, ids_flat)
     _set_device(device)
     st = _stream(device)
-    ws = _ws(_lib.FSA_OP_BWD1, B, k, 0, num_nodes, device, st)
+    ws = _ws(_lib.FSA_OP_BWD1, B, k, 0, num_nodes, device, st, g.shape[1], _DTYPE_CODE[g.dtype])
     _lib.check(_lib.load().fsa_fused_1hop_bwd(
         g.data_ptr(), B, g.shape[1], g.stride(0), _DTYPE_CODE[g.dtype], samples.data_ptr(),
         takes.data_ptr(), k, int(num_nodes), buf.data_ptr(), mode, None, None, None,
@@ -463,7 +464,7 @@ def fused_2hop_backward(grad_out, indices: Optional[SampledIndices2], num_nodes:
         buf, mode = None, 0
     _set_device(device)
     st = _stream(device)
-    ws = _ws(_lib.FSA_OP_BWD2, B, k1, k2, num_nodes, device, st)
+    ws = _ws(_lib.FSA_OP_BWD2, B, k1, k2, num_nodes, device, st, g.shape[1], _DTYPE_CODE[g.dtype])
     _lib.check(_lib.load().fsa_fused_2hop_bwd(
         g.data_ptr(), B, g.shape[1], g.stride(0), _DTYPE_CODE[g.dtype], s1.data_ptr(), s2.data_ptr(),
         k1, k2, int(num_nodes), _ptr(buf), mode, _ptr(touched), _ptr(n_touched), _ptr(grad_rows),

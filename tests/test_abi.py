@@ -44,12 +44,19 @@ def test_host_only_entry_points(lib):
     assert b"sm_100a" in lib.fsa_version()
     assert lib.fsa_status_string(0) == b"ok"
     assert lib.fsa_status_string(_lib.FSA_ERR_WORKSPACE) == b"workspace too small"
-    for op, args in ((_lib.FSA_OP_FWD1, (1024, 10, 0, 0)), (_lib.FSA_OP_FWD2, (1024, 15, 10, 0)),
-                     (_lib.FSA_OP_BWD1, (1024, 10, 0, 10000)), (_lib.FSA_OP_BWD2, (1024, 15, 10, 2449029))):
+    F32, F64 = _lib.FSA_F32, _lib.FSA_F64
+    for op, args in ((_lib.FSA_OP_FWD1, (1024, 10, 0, 0, 0, 0)), (_lib.FSA_OP_FWD2, (1024, 15, 10, 0, 0, 0)),
+                     (_lib.FSA_OP_BWD1, (1024, 10, 0, 100, F32, 10000)),
+                     (_lib.FSA_OP_BWD2, (1024, 15, 10, 100, F32, 2449029))):
         assert lib.fsa_ws_bytes(op, *args) > 0
-    assert lib.fsa_ws_bytes(_lib.FSA_OP_FWD2, 1024, 15, 0, 0) == 0  # k2 < 1
-    # bwd workspace grows with N (persistent per-node counters)
-    assert lib.fsa_ws_bytes(_lib.FSA_OP_BWD2, 64, 4, 4, 10**6) > lib.fsa_ws_bytes(_lib.FSA_OP_BWD2, 64, 4, 4, 10)
+    assert lib.fsa_ws_bytes(_lib.FSA_OP_FWD2, 1024, 15, 0, 0, 0, 0) == 0  # k2 < 1
+    assert lib.fsa_ws_bytes(_lib.FSA_OP_BWD2, 64, 4, 4, 0, F32, 100) == 0  # D < 1
+    assert lib.fsa_ws_bytes(_lib.FSA_OP_BWD2, 64, 4, 4, 8, 99, 100) == 0  # bad dtype
+    # bwd workspace grows with N (persistent per-node counters) and with the term table (G x D)
+    assert lib.fsa_ws_bytes(_lib.FSA_OP_BWD2, 64, 4, 4, 8, F32, 10**6) > lib.fsa_ws_bytes(_lib.FSA_OP_BWD2, 64, 4, 4, 8, F32, 10)
+    small = lib.fsa_ws_bytes(_lib.FSA_OP_BWD2, 64, 4, 4, 8, F32, 10)
+    assert lib.fsa_ws_bytes(_lib.FSA_OP_BWD2, 64, 4, 4, 8 + 256, F32, 10) >= small + 64 * 4 * 256 * 4
+    assert lib.fsa_ws_bytes(_lib.FSA_OP_BWD2, 64, 4, 4, 256, F64, 10) > lib.fsa_ws_bytes(_lib.FSA_OP_BWD2, 64, 4, 4, 256, F32, 10)
 
 
 def test_argument_errors_are_reported_before_any_cuda_call(lib):

@@ -371,8 +371,9 @@ def test_division_hook(fsa):
 
 
 def test_phase_entry_points_equal_monolithic_calls(fsa, golden_powerlaw):
-    """fsa_fused_2hop_fwd_phase (SAMPLE, GATHER) and fsa_fused_2hop_bwd_phase (PLAN, APPLY), the
-    split the step executor schedules across streams, give the monolithic calls' results bitwise."""
+    """fsa_fused_2hop_fwd_phase (SAMPLE, GATHER) and fsa_fused_2hop_bwd_phase (PLAN, TERMS, ROWS
+    in any grouping), the split the step executor schedules across streams, give the monolithic
+    calls' results bitwise."""
     from paper_2511_13645_b200 import _lib
     lib = _lib.load()
     name, c = next(iter_cases(golden_powerlaw))
@@ -383,28 +384,34 @@ def test_phase_entry_points_equal_monolithic_calls(fsa, golden_powerlaw):
     gout = torch.randn((B, D), device="cuda", dtype=X.dtype)
     ref_grad = fsa.fused_2hop_backward(gout, ref_idx, N)
     st = torch.cuda.current_stream().cuda_stream
-    ws_f = torch.zeros(lib.fsa_ws_bytes(_lib.FSA_OP_FWD2, B, k1, k2, 0), dtype=torch.uint8, device="cuda")
-    ws_b = torch.zeros(lib.fsa_ws_bytes(_lib.FSA_OP_BWD2, B, k1, k2, N), dtype=torch.uint8, device="cuda")
+    ws_f = torch.zeros(lib.fsa_ws_bytes(_lib.FSA_OP_FWD2, B, k1, k2, 0, 0, 0), dtype=torch.uint8, device="cuda")
+    code = _lib.FSA_F32 if X.dtype == torch.float32 else _lib.FSA_F64
+    ws_b = torch.zeros(lib.fsa_ws_bytes(_lib.FSA_OP_BWD2, B, k1, k2, D, code, N), dtype=torch.uint8, device="cuda")
     out = torch.empty_like(ref_out)
     s1 = torch.empty((B, k1), dtype=torch.int32, device="cuda")
     s2 = torch.empty((B, k1, k2), dtype=torch.int32, device="cuda")
     t1 = torch.empty(B, dtype=torch.int32, device="cuda")
     t2 = torch.empty((B, k1), dtype=torch.int32, device="cuda")
-    code = _lib.FSA_F32 if X.dtype == torch.float32 else _lib.FSA_F64
     for phase in (_lib.FSA_FWD_SAMPLE, _lib.FSA_FWD_GATHER):
         _lib.check(lib.fsa_fused_2hop_fwd_phase(
             g.rowptr.data_ptr(), g.col.data_ptr(), N, X.data_ptr(), D, X.stride(0), code, seeds.data_ptr(), B, 0,
             k1, k2, c["base_seed"] & (2**64 - 1), None, 1, s1.data_ptr(), s2.data_ptr(), t1.data_ptr(),
             t2.data_ptr(), out.data_ptr(), out.stride(0), ws_f.data_ptr(), ws_f.numel(), st, phase), "fwd phase")
-    grad = torch.zeros((N, D), device="cuda", dtype=X.dtype)
-    for phase in (_lib.FSA_BWD_PLAN, _lib.FSA_BWD_APPLY):
-        _lib.check(lib.fsa_fused_2hop_bwd_phase(
-            gout.data_ptr(), B, D, D, code, s1.data_ptr(), s2.data_ptr(), k1, k2, N, grad.data_ptr(), 0, None, None,
-            None, ws_b.data_ptr(), ws_b.numel(), st, phase), "bwd phase")
-    torch.cuda.synchronize()
     assert torch.equal(s1, ref_idx.s1) and torch.equal(s2, ref_idx.s2)
     assert torch.equal(out, ref_out)
-    assert torch.equal(grad, ref_grad)
+    P, Tm, R = _lib.FSA_BWD_PLAN, _lib.FSA_BWD_TERMS, _lib.FSA_BWD_ROWS
+    for split in ((P, _lib.FSA_BWD_APPLY), (P | Tm, R), (P, Tm, R), (Tm, P, R)):
+        grad = torch.zeros((N, D), device="cuda", dtype=X.dtype)
+        for phase in split:  # grad_out is only needed from TERMS on
+            _lib.check(lib.fsa_fused_2hop_bwd_phase(
+                gout.data_ptr() if phase & Tm else None, B, D, D, code, s1.data_ptr(), s2.data_ptr(), k1, k2, N,
+                grad.data_ptr(), 0, None, None, None, ws_b.data_ptr(), ws_b.numel(), st, phase), "bwd phase")
+        torch.cuda.synchronize()
+        assert torch.equal(grad, ref_grad), split
+    with pytest.raises(RuntimeError):  # TERMS without grad_out
+        _lib.check(lib.fsa_fused_2hop_bwd_phase(
+            None, B, D, D, code, s1.data_ptr(), s2.data_ptr(), k1, k2, N, grad.data_ptr(), 0, None, None, None,
+            ws_b.data_ptr(), ws_b.numel(), st, Tm), "bwd phase")
 
 
 @pytest.mark.parametrize("B,leaves", [(40, 64), (1024, 3000)])
