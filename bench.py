@@ -433,11 +433,10 @@ def cpu_model():
 # ----------------------------------------------------------------------------------------------
 def run_fused(args):
     import torch
-    if os.environ.get("FSA_SEG_DIV"):  # experiment knob: sampler bucket-length divisor
-        from paper_2511_13645_b200 import _lib
-        lib = _lib.load()
-        lib.fsa_tune.argtypes = [_lib.C.c_int, _lib.C.c_int]
-        lib.fsa_tune(1, int(os.environ["FSA_SEG_DIV"]))
+    for knob, env in ((1, "FSA_SEG_DIV"), (2, "FSA_GATHER_PREFETCH")):  # experiment knobs (fsa_tune)
+        if os.environ.get(env):
+            from paper_2511_13645_b200 import _lib
+            _lib.check(_lib.load().fsa_tune(knob, int(os.environ[env])), env)
     from paper_2511_13645_b200 import synth
 
     world, rank, local = dist_env()

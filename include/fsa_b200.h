@@ -220,6 +220,10 @@ int fsa_div_check(int dmax, unsigned long long* mismatches, void* stream);
 /* Micro-benchmark of the sampler's draw loop: one warp of `lanes` lanes, n draws per lane from
  * modulus m0 (mode 0 Barrett, 1 fraction test); out[0] = clock64 cycles, out[1] checksum. */
 int fsa_bench_draws(int mode, int n, uint32_t m0, int k, int lanes, unsigned long long* out, void* stream);
+/* Performance knobs for experiments (results never change): what = 1, the sampler's bucket-length
+ * divisor (value >= 1, default 4); what = 2, the gather's L2 prefetch of a root's rows (0/1,
+ * default 0). */
+int fsa_tune(int what, int value);
 /* out[i] = x[i] % m[i] through the Barrett path used by the sampler (2 <= m <= 2^30) */
 int fsa_umod(const uint64_t* x, const uint32_t* m, int64_t n, uint32_t* out, void* stream);
 

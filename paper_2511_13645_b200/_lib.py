@@ -63,6 +63,7 @@ SIGNATURES = {
     "fsa_umod": (_int, [_p, _p, _i64, _p, _p]),
     "fsa_div_check": (_int, [_int, _p, _p]),
     "fsa_bench_draws": (_int, [_int, _int, C.c_uint32, _int, _int, _p, _p]),
+    "fsa_tune": (_int, [_int, _int]),
 }
 
 _LIB = None

@@ -55,6 +55,7 @@ class Fused2HopStep:
         self.dtype = X.dtype
         self.code = _DTYPE_CODE[X.dtype]
         self.use_graph, self.overlap_zero = use_graph, overlap_zero
+        self.sched = os.environ.get("FSA_SCHED", "overlap")  # experiment: "plan_first"
         dev = self.device
         lib = _lib.load()
         _set_device(dev)
@@ -116,10 +117,14 @@ class Fused2HopStep:
             return
         # the backward does not read the gather's output: PLAN -> ROWS run as one branch beside it
         ps = self.plan
-        ps.wait_stream(main)
         zs.wait_stream(main)  # TERMS after the re-zeroing, on the same side stream
         _lib.check(lib.fsa_fused_2hop_bwd_phase(*bwd_args, zs.cuda_stream, _lib.FSA_BWD_TERMS), "bwd TERMS")
-        _lib.check(lib.fsa_fused_2hop_bwd_phase(*bwd_args, ps.cuda_stream, _lib.FSA_BWD_PLAN), "bwd PLAN")
+        if self.sched == "plan_first":  # PLAN ahead of the gather; ROWS then overlaps the gather
+            _lib.check(lib.fsa_fused_2hop_bwd_phase(*bwd_args, st, _lib.FSA_BWD_PLAN), "bwd PLAN")
+            ps.wait_stream(main)
+        else:
+            ps.wait_stream(main)
+            _lib.check(lib.fsa_fused_2hop_bwd_phase(*bwd_args, ps.cuda_stream, _lib.FSA_BWD_PLAN), "bwd PLAN")
         _lib.check(lib.fsa_fused_2hop_fwd_phase(*fwd_args, _lib.FSA_FWD_GATHER), "fwd GATHER")
         ps.wait_stream(zs)  # term table written, previous rows zeroed
         _lib.check(lib.fsa_fused_2hop_bwd_phase(*bwd_args, ps.cuda_stream, _lib.FSA_BWD_ROWS), "bwd ROWS")
