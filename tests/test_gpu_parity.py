@@ -439,3 +439,41 @@ def test_hub_hit_by_every_slot(fsa, oracle_mod, B, leaves):
     assert np.array_equal(idx.s2.cpu().numpy(), s2)
     assert bitwise(out, ref_out)
     assert bitwise(grad, ref_grad)
+
+
+@pytest.mark.parametrize("D,dtype", [(300, torch.float32), (602, torch.bfloat16), (37, torch.float64),
+                                     (130, torch.float16)])
+def test_wide_rows_dense_collisions(fsa, oracle_mod, D, dtype):
+    """A small random graph with wide rows: most second-hop nodes are hit several times, so
+    every row writer runs on rows wider than one warp's chunk span (the multi-hit kernel's wide
+    path, many term-table chunks per group), with dense and COO outputs — bitwise against the
+    oracle on the same (rounded) inputs."""
+    rng = np.random.default_rng(D)
+    n, deg = 3000, 40  # every row also lists node 0: a hub next to ~13-hit ordinary nodes
+    col = np.stack([np.concatenate([[0], np.sort(rng.choice(np.arange(1, n), deg - 1, replace=False))])
+                    for _ in range(n)]).astype(np.int32).ravel()
+    rowptr = np.arange(0, n * deg + 1, deg, dtype=np.int64)
+    g = dev_graph(fsa, rowptr, col, n)
+    Xd = T(rng.standard_normal((n, D)).astype(np.float32)).to(dtype)
+    seeds = rng.integers(0, n, 256).astype(np.int64)
+    k1, k2, bs = 15, 10, 987654321
+    out, idx = fsa.fused_2hop_forward(g, Xd, T(seeds), k1, k2, bs)
+    gout = T(rng.standard_normal((256, D)).astype(np.float32)).to(dtype)
+    T2 = idx.s2.numel()
+    touched = torch.empty(T2, dtype=torch.int32, device="cuda")
+    nt = torch.empty(1, dtype=torch.int32, device="cuda")
+    rows = torch.empty((T2, D), device="cuda", dtype=dtype)
+    grad = fsa.fused_2hop_backward(gout, idx, n, touched=touched, n_touched=nt, grad_rows=rows)
+    torch.cuda.synchronize()
+    acc = np.float64 if dtype == torch.float64 else np.float32
+    ref_out, s1, s2, _, _ = oracle_mod.fused_2hop(rowptr.astype(np.int32), col, Xd.to(torch.float64).cpu().numpy().astype(acc),
+                                                  seeds, k1, k2, bs)
+    ref_grad = oracle_mod.backward_2hop(gout.to(torch.float64).cpu().numpy().astype(acc), s1, s2, n)
+    assert np.array_equal(idx.s2.cpu().numpy(), s2)
+    hits = np.bincount(s2[s2 >= 0], minlength=n)
+    assert (hits > 1).sum() > 100 and hits.max() > 32  # multi-hit and hub paths both exercised
+    assert torch.equal(out, torch.from_numpy(ref_out).cuda().to(dtype))
+    assert torch.equal(grad, torch.from_numpy(ref_grad).cuda().to(dtype))
+    k = int(nt)
+    assert k == int((hits > 0).sum())
+    assert torch.equal(rows[:k], grad[touched[:k].long()])
