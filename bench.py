@@ -488,7 +488,9 @@ def run_fused(args):
     dom_ms = prof[dom][0]
     kb = kernel_alg_bytes(dom, B, k1, k2, D, E, main["T1"], main["T2"], main["U2"], main["singles"])
     achieved = kb / (dom_ms / 1e3) / 1e9 if kb else None
-    traffic, traffic_src = ncu_traffic(dom)
+    # the committed capture is of the products alpha=3 step (tools/profile_step.py defaults)
+    traffic, traffic_src = ncu_traffic(dom) if (args.config == "products" and args.alpha == 3.0
+                                                and E == 4) else (None, None)
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "traffic_source": traffic_src, "alg_bytes_per_launch": kb,

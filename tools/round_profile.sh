@@ -11,6 +11,11 @@ timeout 900 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_
 timeout 300 python tools/timeline.py --reps 2 > gpurun_out/${TAG}_timeline.txt 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv \
     python tools/profile_step.py --alpha 3.0 --steps 3 > /dev/null 2>&1
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_ -s 11 -c 11 \
+# one step = 6 forward + 8 backward launches (with the sparse re-zero); skip the first step
+NK=${NK:-14}
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_ -s $NK -c $NK \
     -o gpurun_out/${TAG}_full -f python tools/profile_step.py --alpha 3.0 --steps 3 > gpurun_out/${TAG}_ncu.log 2>&1
+python tools/ncu_traffic.py gpurun_out/${TAG}_full.ncu-rep ${TAG} > gpurun_out/${TAG}_ncu_traffic.json 2>&1
+timeout 600 python bench.py --config reddit --no-cpu --no-alt > gpurun_out/${TAG}_bench_reddit.json 2>&1
+timeout 600 python bench.py --config arxiv --no-cpu --no-alt > gpurun_out/${TAG}_bench_arxiv.json 2>&1
 ls gpurun_out | grep ${TAG}
