@@ -473,7 +473,9 @@ def test_wide_rows_dense_collisions(fsa, oracle_mod, D, dtype):
     hits = np.bincount(s2[s2 >= 0], minlength=n)
     assert (hits > 1).sum() > 100 and hits.max() > 32  # multi-hit and hub paths both exercised
     assert torch.equal(out, torch.from_numpy(ref_out).cuda().to(dtype))
-    assert torch.equal(grad, torch.from_numpy(ref_grad).cuda().to(dtype))
+    want = torch.from_numpy(ref_grad).cuda().to(dtype)
+    bad = (grad != want).any(1).nonzero().flatten().tolist()
+    assert not bad, (bad[:8], hits[bad[:8]].tolist())
     k = int(nt)
     assert k == int((hits > 0).sum())
     assert torch.equal(rows[:k], grad[touched[:k].long()])
