@@ -51,6 +51,7 @@ def parse_args():
     p.add_argument("--dtype", default=None, choices=[None, "fp32", "bf16"])
     p.add_argument("--seed", type=int, default=42)
     p.add_argument("--no-alt", action="store_true", help="skip the alpha=2.1 side measurement")
+    p.add_argument("--no-unfused", action="store_true", help="skip the unfused-comparator measurement")
     p.add_argument("--cpu-seconds", type=float, default=10.0)
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--profile", action="store_true", help="print the per-kernel table to stderr")
@@ -381,6 +382,40 @@ class Runner:
         return ms, 8 * self.B + self.E * self.B * self.D, self.E * self.B * self.D
 
 
+    def per_call(self, steps, warmup, impl):
+        """Device time of one fwd+bwd through the per-call API with device-resident inputs:
+        impl "fused" (fused_2hop_forward/backward) or "unfused" / "unfused_dedup" (the
+        materialised comparator, baseline.py).  Both re-zero the gradient sparsely.  Returns
+        (ms per step, bytes the unfused block and gradient block materialise per step)."""
+        torch, fsa = self.torch, self.fsa
+        extra = [0]
+
+        def one(i):
+            seeds = self.batches[i % len(self.batches)]
+            if impl == "fused":
+                _, idx = fsa.fused_2hop_forward(self.g, self.X, seeds, self.k1, self.k2, self.base_seeds[i],
+                                                validate=False, root_offset=self.root_offset)
+                fsa.fused_2hop_backward(self.gout, idx, self.N, out=self.gbuf, validate=False, zero="sparse")
+            else:
+                _, blk = fsa.baseline_forward(self.g, self.X, seeds, self.k1, self.k2, self.base_seeds[i],
+                                              dedup=impl == "unfused_dedup", validate=False,
+                                              root_offset=self.root_offset)
+                fsa.baseline_backward(self.gout, blk, self.N, out=self.gbuf, zero="sparse", validate=False)
+                acc = 8 if self.dtype == torch.float64 else 4
+                extra[0] = blk.nbytes() + blk.ids2.numel() * (-(-self.D // 8) * 8) * acc  # + gradient block
+
+        for i in range(warmup):
+            one(i)
+        torch.cuda.synchronize(self.device)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for j in range(steps):
+            one(warmup + j)
+        b.record()
+        torch.cuda.synchronize(self.device)
+        return a.elapsed_time(b) / steps, extra[0]
+
+
 def max_over_ranks(x, world, device):
     if world == 1:
         return x
@@ -469,6 +504,9 @@ def run_fused(args):
             res["prof"] = r.profile()
             res["e2e"] = r.e2e(max(20, args.steps // 2), 3)
             res["e2e_eager"] = r.e2e_eager(max(20, args.steps // 2), 3)
+            if not args.no_unfused:
+                res["per_call"] = {impl: r.per_call(max(20, args.steps // 4), 3, impl)
+                                   for impl in ("fused", "unfused", "unfused_dedup")}
         return res
 
     main = measure(args.alpha)
@@ -558,6 +596,17 @@ def run_fused(args):
                                  "path": "fused_2hop_forward + fused_2hop_backward(zero='sparse') per call"}},
         "p50_ms": round(main["p50"], 5),
     }
+    if "per_call" in main:  # the paper's comparison: fused vs the materialised pipeline, same API level
+        pc = main["per_call"]
+        fused_ms = pc["fused"][0]
+        line["unfused_comparator"] = {
+            "path": "per-call API, device-resident inputs, sparse gradient re-zero: fused_2hop_forward/backward "
+                    "vs baseline_forward/backward (materialised blocks, baseline.py)",
+            "fused": {"ms_per_step": round(fused_ms, 5), "value": round(world * B / (fused_ms / 1e3), 1)},
+            **{impl: {"ms_per_step": round(pc[impl][0], 5), "value": round(world * B / (pc[impl][0] / 1e3), 1),
+                      "speedup_of_fused": round(pc[impl][0] / fused_ms, 3),
+                      "materialised_bytes_per_step": pc[impl][1]} for impl in ("unfused", "unfused_dedup")},
+            "unit": "seeds/s"}
     if rank == 0 and not args.no_cpu:
         times, threads = cpu_oracle_time(r, args.cpu_seconds, max_steps=30)
         cpu_ms = statistics.median(times) * 1e3

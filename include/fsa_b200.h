@@ -220,6 +220,30 @@ int fsa_div_check(int dmax, unsigned long long* mismatches, void* stream);
 /* Micro-benchmark of the sampler's draw loop: one warp of `lanes` lanes, n draws per lane from
  * modulus m0 (mode 0 Barrett, 1 fraction test); out[0] = clock64 cycles, out[1] checksum. */
 int fsa_bench_draws(int mode, int n, uint32_t m0, int k, int lanes, unsigned long long* out, void* stream);
+/* ---- unfused comparator (baseline.py:63-194): the same sums with every intermediate in HBM ----
+ * fsa_gather_rows: out[t] = X[ids[t]] (zero row for -1)                 (kernels.gather_rows)
+ * fsa_group_mean:  out[g] = (+0 + sum_{l < take[g]} row(g*k + l)) / max(1, take[g]) with
+ *                  row(i) = src[remap ? remap[i] : i]; src_acc / out_acc select the accumulation
+ *                  type (fp32, fp64 for FSA_F64) instead of `dtype` for src / out rows
+ *                  (kernels.agg_1hop_block, partials_2hop_block/_dedup, agg_2hop_from_partials)
+ * fsa_baseline_*_bwd: the replay backward with the per-slot gradient block materialised in
+ *                  d_gathered [B*k(1*k2)][dg_stride] (accumulation type, dg_stride a multiple of 8
+ *                  and >= D, 16-B aligned) between the division and the ordered scatter
+ *                  (kernels.expand_grad + scatter_from_block); same workspace as fsa_fused_*_bwd. */
+int fsa_gather_rows(const void* X, int64_t D, int64_t x_stride, int dtype, const int32_t* ids, int64_t n,
+                    void* out, int64_t out_stride, void* stream);
+int fsa_group_mean(const void* src, int64_t src_stride, int src_acc, const int32_t* remap, const int32_t* take,
+                   int32_t k, int64_t G, int64_t D, int dtype, void* out, int64_t out_stride, int out_acc,
+                   void* stream);
+int fsa_baseline_1hop_bwd(const void* grad_out, int64_t B, int64_t D, int64_t g_stride, int dtype,
+                          const int32_t* samples, const int32_t* takes, int32_t k, int64_t N, void* grad_x,
+                          int zero_mode, void* d_gathered, int64_t dg_stride, void* ws, size_t ws_bytes,
+                          void* stream);
+int fsa_baseline_2hop_bwd(const void* grad_out, int64_t B, int64_t D, int64_t g_stride, int dtype,
+                          const int32_t* s1, const int32_t* s2, int32_t k1, int32_t k2, int64_t N, void* grad_x,
+                          int zero_mode, void* d_gathered, int64_t dg_stride, void* ws, size_t ws_bytes,
+                          void* stream);
+
 /* Performance knobs for experiments (results never change): what = 1, the sampler's bucket-length
  * divisor (value >= 1, default 4); what = 2, the gather's L2 prefetch of a root's rows (0/1,
  * default 0). */

@@ -8,6 +8,7 @@ from .autograd import (
     fused_sample_agg_1hop,
     fused_sample_agg_2hop,
 )
+from .baseline import MaterializedBlock, baseline_1hop_forward, baseline_backward, baseline_forward
 from .fused import (
     SampledIndices1,
     SampledIndices2,
@@ -24,6 +25,10 @@ from .graph import CsrGraph, SeedBatch
 from .rng import RngStream, derive_stream, splitmix64, step_seed, xorshift64
 
 __all__ = [
+    "MaterializedBlock",
+    "baseline_1hop_forward",
+    "baseline_forward",
+    "baseline_backward",
     "CsrGraph",
     "SeedBatch",
     "SampledIndices1",

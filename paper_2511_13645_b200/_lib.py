@@ -64,6 +64,11 @@ SIGNATURES = {
     "fsa_div_check": (_int, [_int, _p, _p]),
     "fsa_bench_draws": (_int, [_int, _int, C.c_uint32, _int, _int, _p, _p]),
     "fsa_tune": (_int, [_int, _int]),
+    "fsa_gather_rows": (_int, [_p, _i64, _i64, _int, _p, _i64, _p, _i64, _p]),
+    "fsa_group_mean": (_int, [_p, _i64, _int, _p, _p, _i32, _i64, _i64, _int, _p, _i64, _int, _p]),
+    "fsa_baseline_1hop_bwd": (_int, [_p, _i64, _i64, _i64, _int, _p, _p, _i32, _i64, _p, _int, _p, _i64, _p, _sz, _p]),
+    "fsa_baseline_2hop_bwd": (_int, [_p, _i64, _i64, _i64, _int, _p, _p, _i32, _i32, _i64, _p, _int, _p, _i64, _p,
+                                      _sz, _p]),
 }
 
 _LIB = None

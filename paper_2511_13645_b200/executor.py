@@ -117,6 +117,15 @@ class Fused2HopStep:
             return
         # the backward does not read the gather's output: PLAN -> ROWS run as one branch beside it
         ps = self.plan
+        if self.sched == "all_first":  # PLAN and TERMS ahead of the gather; ROWS overlaps the gather
+            _lib.check(lib.fsa_fused_2hop_bwd_phase(*bwd_args, st, _lib.FSA_BWD_PLAN), "bwd PLAN")
+            _lib.check(lib.fsa_fused_2hop_bwd_phase(*bwd_args, st, _lib.FSA_BWD_TERMS), "bwd TERMS")
+            ps.wait_stream(main)
+            _lib.check(lib.fsa_fused_2hop_fwd_phase(*fwd_args, _lib.FSA_FWD_GATHER), "fwd GATHER")
+            ps.wait_stream(zs)
+            _lib.check(lib.fsa_fused_2hop_bwd_phase(*bwd_args, ps.cuda_stream, _lib.FSA_BWD_ROWS), "bwd ROWS")
+            main.wait_stream(ps)
+            return
         zs.wait_stream(main)  # TERMS after the re-zeroing, on the same side stream
         _lib.check(lib.fsa_fused_2hop_bwd_phase(*bwd_args, zs.cuda_stream, _lib.FSA_BWD_TERMS), "bwd TERMS")
         if self.sched == "plan_first":  # PLAN ahead of the gather; ROWS then overlaps the gather
