@@ -21,7 +21,7 @@ from .fused import (
     sample_2hop,
     sample_neighbors_reservoir,
 )
-from .graph import CsrGraph, SeedBatch
+from .graph import CsrGraph, GraphFormatError, SeedBatch, load_csr_cache, save_csr_cache
 from .rng import RngStream, derive_stream, splitmix64, step_seed, xorshift64
 
 __all__ = [
@@ -31,6 +31,9 @@ __all__ = [
     "baseline_backward",
     "CsrGraph",
     "SeedBatch",
+    "GraphFormatError",
+    "save_csr_cache",
+    "load_csr_cache",
     "SampledIndices1",
     "SampledIndices2",
     "fused_1hop_forward",

@@ -9,6 +9,7 @@ HBM as torch int32 tensors; any reference-style graph object (``num_nodes``, num
 
 from __future__ import annotations
 
+import os
 import weakref
 from dataclasses import dataclass
 from typing import Optional, Union
@@ -18,7 +19,14 @@ import torch
 
 MAX_NODES = 2**31 - 1
 
-__all__ = ["CsrGraph", "SeedBatch", "as_device_graph", "as_seed_tensor"]
+__all__ = ["CsrGraph", "SeedBatch", "GraphFormatError", "as_device_graph", "as_seed_tensor", "save_csr_cache",
+           "load_csr_cache"]
+
+CACHE_MAGIC = b"FSA1"
+
+
+class GraphFormatError(ValueError):
+    """Malformed graph file (graph.py:30-31)."""
 
 
 @dataclass(frozen=True, eq=False)
@@ -150,3 +158,41 @@ def as_seed_tensor(seeds, device: torch.device) -> torch.Tensor:
     if t.ndim != 1 or t.numel() == 0:
         raise ValueError("seed batch must be a non-empty 1-D array")
     return t.to(device, non_blocking=True)
+
+
+# ---- FSA1 binary CSR cache (graph.py:266-292), byte-compatible with the reference -------------
+def save_csr_cache(graph, path) -> None:
+    """Write the binary CSR cache: magic "FSA1", N (u64 LE), rowptr, col (i32 LE)."""
+    if isinstance(graph, CsrGraph):
+        rowptr, col = graph.cpu_arrays()
+        n = graph.num_nodes
+    else:
+        rowptr, col, n = np.asarray(graph.rowptr), np.asarray(graph.col), int(graph.num_nodes)
+    with open(path, "wb") as fh:
+        fh.write(CACHE_MAGIC)
+        fh.write(np.uint64(n).astype("<u8").tobytes())
+        fh.write(np.ascontiguousarray(rowptr, dtype="<i4").tobytes())
+        fh.write(np.ascontiguousarray(col, dtype="<i4").tobytes())
+
+
+def load_csr_cache(path, device: Union[str, torch.device, None] = None) -> CsrGraph:
+    """Read an FSA1 cache into a device graph (same checks and messages as graph.py:276-292)."""
+    size = os.path.getsize(path)
+    with open(path, "rb") as fh:
+        magic = fh.read(4)
+        if magic != CACHE_MAGIC:
+            raise GraphFormatError(f"{path}: bad magic {magic!r}, expected {CACHE_MAGIC!r}")
+        hdr = fh.read(8)
+        if len(hdr) != 8:
+            raise GraphFormatError(f"{path}: truncated header")
+        n = int(np.frombuffer(hdr, dtype="<u8")[0])
+        if n == 0 or n > MAX_NODES:
+            raise GraphFormatError(f"{path}: implausible node count {n}")
+        if size < 12 + 4 * (n + 1):
+            raise GraphFormatError(f"{path}: truncated rowptr")
+        rowptr = np.fromfile(fh, dtype="<i4", count=n + 1)
+        nnz = int(rowptr[-1])
+        if nnz < 0 or size < 12 + 4 * (n + 1) + 4 * nnz:
+            raise GraphFormatError(f"{path}: truncated col")
+        col = np.fromfile(fh, dtype="<i4", count=nnz)
+    return CsrGraph.from_arrays(rowptr.astype(np.int32), col.astype(np.int32), device=device, num_nodes=n)
