@@ -56,8 +56,8 @@ def test_train_step_matches_reference_math(oracle_mod, golden_powerlaw):
         seeds = rng.integers(0, N, size=48)
         y = rng.integers(0, 5, size=48)
         bs = fsa.step_seed(42, step)
-        res = train.train_step(g, Xd, torch.as_tensor(seeds).cuda(), torch.as_tensor(y).cuda(), (c["k1"], c["k2"]),
-                               bs, state, grad_scratch=gbuf)
+        res = train.train_step(g, Xd, fsa.SeedBatch(seeds, y), (c["k1"], c["k2"]), bs, "fused", state,
+                               grad_scratch=gbuf)
         out, s1, s2, _, _ = oracle_mod.fused_2hop(c["rowptr"].astype(np.int32), c["col"].astype(np.int32), X, seeds,
                                                   c["k1"], c["k2"], bs)
         loss, dxa = ref_step(X[seeds].astype(np.float64), out.astype(np.float64), y, P, M, V, step + 1)
@@ -80,3 +80,31 @@ def test_nonfinite_gradient_skips_the_update():
     assert not bool(ok)
     for k in train.PARAM_NAMES:
         assert torch.equal(getattr(state, k), before[k])
+
+
+@pytest.mark.parametrize("dedup", [False, True])
+def test_baseline_variant_trains_identically(golden_powerlaw, dedup):
+    """train_step(variant="baseline") (the materialised comparator) gives the same losses,
+    parameters and feature gradients as variant="fused", step after step (train.py:185-251)."""
+    import paper_2511_13645_b200 as fsa
+    from paper_2511_13645_b200 import train
+
+    name, c = next(iter_cases(golden_powerlaw))
+    N, D = c["N"], c["X"].shape[1]
+    g = fsa.CsrGraph.from_arrays(c["rowptr"], c["col"], device="cuda", num_nodes=N)
+    Xd = torch.as_tensor(c["X"].astype(np.float32)).cuda()
+    states = [train.init_train_state(D, 32, 5, base_seed=7) for _ in range(2)]
+    bufs = [torch.zeros((N, D), device="cuda") for _ in range(2)]
+    rng = np.random.default_rng(4)
+    for step in range(3):
+        batch = fsa.SeedBatch(rng.integers(0, N, size=40), rng.integers(0, 5, size=40))
+        bs = fsa.step_seed(7, step)
+        rf = train.train_step(g, Xd, batch, (c["k1"], c["k2"]), bs, "fused", states[0], grad_scratch=bufs[0])
+        rb = train.train_step(g, Xd, batch, (c["k1"], c["k2"]), bs, "baseline", states[1], grad_scratch=bufs[1],
+                              dedup=dedup)
+        assert torch.equal(rf.loss, rb.loss) and rf.sampled_pairs == rb.sampled_pairs
+        assert torch.equal(bufs[0], bufs[1])
+        for k in train.PARAM_NAMES:
+            assert torch.equal(getattr(states[0], k), getattr(states[1], k))
+    with pytest.raises(ValueError, match="variant"):
+        train.train_step(g, Xd, batch, (c["k1"], c["k2"]), 1, "unfused", states[0])
