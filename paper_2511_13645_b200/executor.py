@@ -14,8 +14,8 @@ work:
   concurrently with the (latency-bound) forward; two graphs alternate s2 buffers so the side
   stream reads the previous step's ids while the forward writes the current ones;
 * the replay backward's PLAN phase (per-node counts, segments: it reads only the sampled ids)
-  runs on a second side stream concurrently with the forward's feature gather; only its APPLY
-  phase (the row writes) waits for the gather.
+  and its row writes run as one branch beside the forward's feature gather (they never read
+  its output); the term table (TERMS) is built on the re-zeroing stream.
 
 Results are bitwise identical to the eager API (tests/test_gpu_executor.py).
 """
@@ -55,7 +55,6 @@ class Fused2HopStep:
         self.dtype = X.dtype
         self.code = _DTYPE_CODE[X.dtype]
         self.use_graph, self.overlap_zero = use_graph, overlap_zero
-        self.sched = os.environ.get("FSA_SCHED", "overlap")  # experiment: "plan_first"
         dev = self.device
         lib = _lib.load()
         _set_device(dev)
@@ -84,10 +83,15 @@ class Fused2HopStep:
         self.steps_run = 0
 
     # -- raw launch sequence of one step (eager or under capture) ----------------------------
-    def _launch(self, parity: int) -> None:
+    def _launch(self, parity: int, head=None, tail=None) -> None:
         """main:   fwd SAMPLE ──┬── fwd GATHER ─────────────────────┬── (step end)
            plan:                ├── bwd PLAN ──────┬── bwd ROWS ──┘  (PLAN needs only s1/s2)
-           zero:   re-zero prev rows ── bwd TERMS ─┘                 (grad_out + s1/s2)"""
+           zero:   re-zero prev rows ── bwd TERMS ─┘                 (grad_out + s1/s2)
+
+        With ``head`` (a callable run on the main stream after the gather, which writes this
+        parity's grad_out buffer from the forward output: a training step's head), TERMS runs on
+        the main stream after it instead; ``tail`` runs on the main stream beside the row writes
+        (a training step's optimizer update)."""
         lib = _lib.load()
         main = torch.cuda.current_stream(self.device)
         cur, prev = self.s2[parity], self.s2[1 - parity]
@@ -110,40 +114,38 @@ class Fused2HopStep:
                     None, None, self.ws_b.data_ptr(), self.ws_b.numel())
         _lib.check(lib.fsa_fused_2hop_fwd_phase(*fwd_args, _lib.FSA_FWD_SAMPLE), "fwd SAMPLE")
         if not self.overlap_zero:
-            for ph in (_lib.FSA_BWD_PLAN, _lib.FSA_BWD_TERMS):
-                _lib.check(lib.fsa_fused_2hop_bwd_phase(*bwd_args, st, ph), "bwd phase")
+            _lib.check(lib.fsa_fused_2hop_bwd_phase(*bwd_args, st, _lib.FSA_BWD_PLAN), "bwd PLAN")
             _lib.check(lib.fsa_fused_2hop_fwd_phase(*fwd_args, _lib.FSA_FWD_GATHER), "fwd GATHER")
+            if head is not None:
+                head(out, grad_out)
+            _lib.check(lib.fsa_fused_2hop_bwd_phase(*bwd_args, st, _lib.FSA_BWD_TERMS), "bwd TERMS")
             _lib.check(lib.fsa_fused_2hop_bwd_phase(*bwd_args, st, _lib.FSA_BWD_ROWS), "bwd ROWS")
+            if tail is not None:
+                tail()
             return
         # the backward does not read the gather's output: PLAN -> ROWS run as one branch beside it
         ps = self.plan
-        if self.sched == "all_first":  # PLAN and TERMS ahead of the gather; ROWS overlaps the gather
-            _lib.check(lib.fsa_fused_2hop_bwd_phase(*bwd_args, st, _lib.FSA_BWD_PLAN), "bwd PLAN")
+        if head is None:
+            zs.wait_stream(main)  # TERMS after the re-zeroing, on the same side stream
+            _lib.check(lib.fsa_fused_2hop_bwd_phase(*bwd_args, zs.cuda_stream, _lib.FSA_BWD_TERMS), "bwd TERMS")
+        ps.wait_stream(main)
+        _lib.check(lib.fsa_fused_2hop_bwd_phase(*bwd_args, ps.cuda_stream, _lib.FSA_BWD_PLAN), "bwd PLAN")
+        _lib.check(lib.fsa_fused_2hop_fwd_phase(*fwd_args, _lib.FSA_FWD_GATHER), "fwd GATHER")
+        if head is not None:
+            head(out, grad_out)
             _lib.check(lib.fsa_fused_2hop_bwd_phase(*bwd_args, st, _lib.FSA_BWD_TERMS), "bwd TERMS")
             ps.wait_stream(main)
-            _lib.check(lib.fsa_fused_2hop_fwd_phase(*fwd_args, _lib.FSA_FWD_GATHER), "fwd GATHER")
-            ps.wait_stream(zs)
-            _lib.check(lib.fsa_fused_2hop_bwd_phase(*bwd_args, ps.cuda_stream, _lib.FSA_BWD_ROWS), "bwd ROWS")
-            main.wait_stream(ps)
-            return
-        zs.wait_stream(main)  # TERMS after the re-zeroing, on the same side stream
-        _lib.check(lib.fsa_fused_2hop_bwd_phase(*bwd_args, zs.cuda_stream, _lib.FSA_BWD_TERMS), "bwd TERMS")
-        if self.sched == "plan_first":  # PLAN ahead of the gather; ROWS then overlaps the gather
-            _lib.check(lib.fsa_fused_2hop_bwd_phase(*bwd_args, st, _lib.FSA_BWD_PLAN), "bwd PLAN")
-            ps.wait_stream(main)
-        else:
-            ps.wait_stream(main)
-            _lib.check(lib.fsa_fused_2hop_bwd_phase(*bwd_args, ps.cuda_stream, _lib.FSA_BWD_PLAN), "bwd PLAN")
-        _lib.check(lib.fsa_fused_2hop_fwd_phase(*fwd_args, _lib.FSA_FWD_GATHER), "fwd GATHER")
         ps.wait_stream(zs)  # term table written, previous rows zeroed
         _lib.check(lib.fsa_fused_2hop_bwd_phase(*bwd_args, ps.cuda_stream, _lib.FSA_BWD_ROWS), "bwd ROWS")
+        if tail is not None:
+            tail()
         main.wait_stream(ps)
 
-    def _capture(self, parity: int) -> torch.cuda.CUDAGraph:
+    def _capture(self, parity: int, head=None, tail=None) -> torch.cuda.CUDAGraph:
         # warm the launch path once outside capture (device init, function attributes)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            self._launch(parity)
+            self._launch(parity, head, tail)
         return g
 
     @property

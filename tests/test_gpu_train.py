@@ -108,3 +108,36 @@ def test_baseline_variant_trains_identically(golden_powerlaw, dedup):
             assert torch.equal(getattr(states[0], k), getattr(states[1], k))
     with pytest.raises(ValueError, match="variant"):
         train.train_step(g, Xd, batch, (c["k1"], c["k2"]), 1, "unfused", states[0])
+
+
+@pytest.mark.parametrize("use_graph", [True, False])
+def test_graph_train_step_matches_eager(golden_powerlaw, use_graph):
+    """GraphTrainStep (the fused training step as CUDA graphs, device-side step count) against
+    the eager train_step: same losses, parameters, sampled pairs and feature gradients."""
+    import paper_2511_13645_b200 as fsa
+    from paper_2511_13645_b200 import train
+
+    name, c = next(iter_cases(golden_powerlaw))
+    N, D = c["N"], c["X"].shape[1]
+    g = fsa.CsrGraph.from_arrays(c["rowptr"], c["col"], device="cuda", num_nodes=N)
+    Xd = torch.as_tensor(c["X"].astype(np.float32)).cuda()
+    B = 40
+    s_eager, s_graph = (train.init_train_state(D, 32, 5, base_seed=3) for _ in range(2))
+    gbuf = torch.zeros((N, D), device="cuda")
+    gts = train.GraphTrainStep(g, Xd, B, (c["k1"], c["k2"]), s_graph, use_graph=use_graph)
+    rng = np.random.default_rng(8)
+    for step in range(6):
+        seeds = torch.as_tensor(rng.integers(0, N, size=B)).cuda()
+        y = torch.as_tensor(rng.integers(0, 5, size=B)).cuda()
+        bs = fsa.step_seed(3, step)
+        re = train.train_step(g, Xd, fsa.SeedBatch(seeds, y), (c["k1"], c["k2"]), bs, "fused", s_eager,
+                              grad_scratch=gbuf)
+        rg = gts.run(seeds, y, bs)
+        torch.cuda.synchronize()
+        assert int(rg.sampled_pairs) == re.sampled_pairs, step
+        assert abs(float(rg.loss) - float(re.loss)) <= 1e-6 * max(1.0, abs(float(re.loss))), step
+        assert bool(rg.grads_applied)
+        for k in train.PARAM_NAMES:
+            torch.testing.assert_close(getattr(s_graph, k), getattr(s_eager, k), rtol=1e-6, atol=1e-7)
+        torch.testing.assert_close(gts.feature_grad, gbuf, rtol=1e-6, atol=1e-7)
+    assert s_graph.step_count == s_eager.step_count == 6
