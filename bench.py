@@ -52,6 +52,7 @@ def parse_args():
     p.add_argument("--seed", type=int, default=42)
     p.add_argument("--no-alt", action="store_true", help="skip the alpha=2.1 side measurement")
     p.add_argument("--no-unfused", action="store_true", help="skip the unfused-comparator measurement")
+    p.add_argument("--no-train", action="store_true", help="skip the SAGE training-step measurement")
     p.add_argument("--cpu-seconds", type=float, default=10.0)
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--profile", action="store_true", help="print the per-kernel table to stderr")
@@ -382,6 +383,40 @@ class Runner:
         return ms, 8 * self.B + self.E * self.B * self.D, self.E * self.B * self.D
 
 
+    def train(self, steps, warmup, graph_mode, hidden=256, classes=47):
+        """SAGE training step (head H=256, C=47, AdamW) around the fused
+        op: eager train_step, or GraphTrainStep (CUDA graphs).  Device-resident seeds/labels.
+        Returns ms per step."""
+        torch, fsa = self.torch, self.fsa
+        from paper_2511_13645_b200 import train as tr
+        state = tr.init_train_state(self.D, hidden, classes, 42, dtype=torch.float32, device=self.device)
+        gen = torch.Generator(device=self.device)
+        gen.manual_seed(7)
+        labels = torch.randint(0, classes, (self.N,), generator=gen, device=self.device)
+        X = self.X
+        if graph_mode:
+            gts = tr.GraphTrainStep(self.g, X, self.B, (self.k1, self.k2), state, root_offset=self.root_offset)
+        gbuf = torch.zeros((self.N, self.D), dtype=X.dtype, device=self.device)
+
+        def one(i):
+            seeds = self.batches[i % len(self.batches)]
+            if graph_mode:
+                gts.run(seeds, labels[seeds], self.base_seeds[i])
+            else:
+                tr.train_step(self.g, X, fsa.SeedBatch(seeds, labels[seeds]), (self.k1, self.k2), self.base_seeds[i],
+                              "fused", state, grad_scratch=gbuf)
+
+        for i in range(warmup):
+            one(i)
+        torch.cuda.synchronize(self.device)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for j in range(steps):
+            one(warmup + j)
+        b.record()
+        torch.cuda.synchronize(self.device)
+        return a.elapsed_time(b) / steps
+
     def per_call(self, steps, warmup, impl):
         """Device time of one fwd+bwd through the per-call API with device-resident inputs:
         impl "fused" (fused_2hop_forward/backward) or "unfused" / "unfused_dedup" (the
@@ -504,6 +539,8 @@ def run_fused(args):
             res["prof"] = r.profile()
             res["e2e"] = r.e2e(max(20, args.steps // 2), 3)
             res["e2e_eager"] = r.e2e_eager(max(20, args.steps // 2), 3)
+            if not args.no_train and r.dtype == torch.float32:
+                res["train"] = {m: r.train(max(20, args.steps // 4), 3, m == "graph") for m in ("graph", "eager")}
             if not args.no_unfused:
                 res["per_call"] = {impl: r.per_call(max(20, args.steps // 4), 3, impl)
                                    for impl in ("fused", "unfused", "unfused_dedup")}
@@ -596,6 +633,13 @@ def run_fused(args):
                                  "path": "fused_2hop_forward + fused_2hop_backward(zero='sparse') per call"}},
         "p50_ms": round(main["p50"], 5),
     }
+    if "train" in main:  # the caller of the hot path: the SAGE training step around the fused op
+        tr_ms = main["train"]
+        line["train_step"] = {
+            "path": "SAGE head H=256, C=47, cross-entropy, AdamW around the fused op; device-resident batches",
+            "graph": {"ms_per_step": round(tr_ms["graph"], 5), "value": round(world * B / (tr_ms["graph"] / 1e3), 1)},
+            "eager": {"ms_per_step": round(tr_ms["eager"], 5), "value": round(world * B / (tr_ms["eager"] / 1e3), 1)},
+            "unit": "seeds/s"}
     if "per_call" in main:  # the paper's comparison: fused vs the materialised pipeline, same API level
         pc = main["per_call"]
         fused_ms = pc["fused"][0]
