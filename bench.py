@@ -215,7 +215,7 @@ class Runner:
         self.N, self.D = shape.num_nodes, shape.d_feat
         self.B, self.k1, self.k2 = args.batch, shape.k1, shape.k2
         self.root_offset = rank * self.B
-        nsteps = args.warmup + args.steps + 8
+        nsteps = max(args.warmup + args.steps, 64) + 8  # the e2e / per-call legs cycle through them
         gb = synth.seed_batches(self.N, self.B * world, args.seed, device=device)
         self.batches = [next(gb)[self.root_offset:self.root_offset + self.B].contiguous() for _ in range(nsteps)]
         self.base_seeds = [fsa.step_seed(args.seed, i) for i in range(nsteps)]
@@ -243,20 +243,26 @@ class Runner:
             self.flush_buf.fill_(1)
 
     def step(self, i):
-        out, idx = self.ex.run(self.batches[i], self.base_seeds[i])
+        nb = len(self.batches)
+        out, idx = self.ex.run(self.batches[i % nb], self.base_seeds[i % nb])
         self.idx = idx
         return out
 
     def eager_step(self, i):
         """The same step through the public operator API (per-kernel profiling, launch counts)."""
         fsa = self.fsa
-        out, idx = fsa.fused_2hop_forward(self.g, self.X, self.batches[i], self.k1, self.k2, self.base_seeds[i],
+        nb = len(self.batches)
+        out, idx = fsa.fused_2hop_forward(self.g, self.X, self.batches[i % nb], self.k1, self.k2, self.base_seeds[i % nb],
                                           validate=False, root_offset=self.root_offset)
         fsa.fused_2hop_backward(self.gout, idx, self.N, out=self.gbuf, validate=False, zero="sparse")
         return out
 
     def timed(self, steps, warmup, flush=True):
         torch = self.torch
+        # at least 4 untimed steps whatever W is: the executor runs each of its two parities
+        # eagerly once, then captures each parity's graph, and no capture may fall in the
+        # timed region
+        warmup = max(warmup, 4)
         for i in range(warmup):
             self.step(i)
         torch.cuda.synchronize(self.device)
@@ -328,14 +334,13 @@ class Runner:
         """End to end through the public step API (executor.Fused2HopStep.run) with pinned host
         inputs: H2D of the step's seeds and grad_out, the fused fwd + replay bwd, D2H of out."""
         torch = self.torch
-        h_seeds = [b.cpu().pin_memory() for b in self.batches[:warmup + steps]]
+        h_seeds = [b.cpu().pin_memory() for b in self.batches]
         h_gout = self.gout.cpu().pin_memory()
-        h_out = torch.empty((self.B, self.D), dtype=self.dtype).pin_memory()
-
-        h_out = [h_out, torch.empty((self.B, self.D), dtype=self.dtype).pin_memory()]
+        h_out = [torch.empty((self.B, self.D), dtype=self.dtype).pin_memory() for _ in range(2)]
+        nb = len(h_seeds)
 
         def one(i):  # H2D of this step's inputs and D2H of its output ride the executor's copy stream
-            self.ex.run(h_seeds[i], self.base_seeds[i], h_gout, out_host=h_out[i % 2])
+            self.ex.run(h_seeds[i % nb], self.base_seeds[i % nb], h_gout, out_host=h_out[i % 2])
 
         for i in range(warmup):
             one(i)
@@ -356,14 +361,15 @@ class Runner:
     def e2e_eager(self, steps, warmup):
         """Same through the per-call operator API (fused_2hop_forward / fused_2hop_backward)."""
         torch, fsa = self.torch, self.fsa
-        h_seeds = [b.cpu().pin_memory() for b in self.batches[:warmup + steps]]
+        h_seeds = [b.cpu().pin_memory() for b in self.batches]
         h_gout = self.gout.cpu().pin_memory()
         h_out = torch.empty((self.B, self.D), dtype=self.dtype).pin_memory()
+        nb = len(h_seeds)
 
         def one(i):
-            seeds = h_seeds[i].to(self.device, non_blocking=True)
+            seeds = h_seeds[i % nb].to(self.device, non_blocking=True)
             gout = h_gout.to(self.device, non_blocking=True)
-            out, idx = fsa.fused_2hop_forward(self.g, self.X, seeds, self.k1, self.k2, self.base_seeds[i],
+            out, idx = fsa.fused_2hop_forward(self.g, self.X, seeds, self.k1, self.k2, self.base_seeds[i % nb],
                                               validate=False, root_offset=self.root_offset)
             fsa.fused_2hop_backward(gout, idx, self.N, out=self.gbuf, validate=False, zero="sparse")
             h_out.copy_(out, non_blocking=True)
@@ -401,9 +407,10 @@ class Runner:
         def one(i):
             seeds = self.batches[i % len(self.batches)]
             if graph_mode:
-                gts.run(seeds, labels[seeds], self.base_seeds[i])
+                gts.run(seeds, labels[seeds], self.base_seeds[i % len(self.base_seeds)])
             else:
-                tr.train_step(self.g, X, fsa.SeedBatch(seeds, labels[seeds]), (self.k1, self.k2), self.base_seeds[i],
+                tr.train_step(self.g, X, fsa.SeedBatch(seeds, labels[seeds]), (self.k1, self.k2),
+                              self.base_seeds[i % len(self.base_seeds)],
                               "fused", state, grad_scratch=gbuf)
 
         for i in range(warmup):
@@ -428,11 +435,13 @@ class Runner:
         def one(i):
             seeds = self.batches[i % len(self.batches)]
             if impl == "fused":
-                _, idx = fsa.fused_2hop_forward(self.g, self.X, seeds, self.k1, self.k2, self.base_seeds[i],
+                _, idx = fsa.fused_2hop_forward(self.g, self.X, seeds, self.k1, self.k2,
+                                                self.base_seeds[i % len(self.base_seeds)],
                                                 validate=False, root_offset=self.root_offset)
                 fsa.fused_2hop_backward(self.gout, idx, self.N, out=self.gbuf, validate=False, zero="sparse")
             else:
-                _, blk = fsa.baseline_forward(self.g, self.X, seeds, self.k1, self.k2, self.base_seeds[i],
+                _, blk = fsa.baseline_forward(self.g, self.X, seeds, self.k1, self.k2,
+                                              self.base_seeds[i % len(self.base_seeds)],
                                               dedup=impl == "unfused_dedup", validate=False,
                                               root_offset=self.root_offset)
                 fsa.baseline_backward(self.gout, blk, self.N, out=self.gbuf, zero="sparse", validate=False)
@@ -540,7 +549,7 @@ def run_fused(args):
             res["e2e"] = r.e2e(max(20, args.steps // 2), 3)
             res["e2e_eager"] = r.e2e_eager(max(20, args.steps // 2), 3)
             if not args.no_train and r.dtype == torch.float32:
-                res["train"] = {m: r.train(max(20, args.steps // 4), 3, m == "graph") for m in ("graph", "eager")}
+                res["train"] = {m: r.train(max(20, args.steps // 4), 5, m == "graph") for m in ("graph", "eager")}
             if not args.no_unfused:
                 res["per_call"] = {impl: r.per_call(max(20, args.steps // 4), 3, impl)
                                    for impl in ("fused", "unfused", "unfused_dedup")}
