@@ -512,7 +512,7 @@ def cpu_model():
 # ----------------------------------------------------------------------------------------------
 def run_fused(args):
     import torch
-    for knob, env in ((1, "FSA_SEG_DIV"), (2, "FSA_GATHER_PREFETCH"), (3, "FSA_ZERO_CTAS"), (4, "FSA_COUNT_CTAS")):  # experiment knobs (fsa_tune)
+    for knob, env in ((1, "FSA_SEG_DIV"), (2, "FSA_GATHER_PREFETCH"), (3, "FSA_ZERO_CTAS"), (4, "FSA_COUNT_CTAS"), (5, "FSA_MULTI_CTAS")):  # experiment knobs (fsa_tune)
         if os.environ.get(env):
             from paper_2511_13645_b200 import _lib
             _lib.check(_lib.load().fsa_tune(knob, int(os.environ[env])), env)
