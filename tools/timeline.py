@@ -28,15 +28,19 @@ def main():
     p.add_argument("--config", default="products")
     p.add_argument("--eager", action="store_true")
     p.add_argument("--reps", type=int, default=3)
-    p.add_argument("--noatomic", action="store_true")
+    p.add_argument("--dtype", default=None, choices=["f32", "bf16"], help="default: bf16 for reddit, else f32")
     a = p.parse_args()
+    bf16 = a.dtype == "bf16" or (a.dtype is None and a.config == "reddit")
     sh = synth.SHAPES[a.config]
     dev = torch.device("cuda", 0)
     g = synth.gen_power_law(sh.num_nodes, sh.avg_degree, a.alpha, 42, device=dev)
     X = synth.make_features(sh.num_nodes, sh.d_feat, 42, device=dev)
+    if bf16:  # 16-byte row stride, as bench.py does
+        stride = -(-sh.d_feat * 2 // 16) * 16 // 2
+        X = synth.make_features(sh.num_nodes, sh.d_feat, 42, dtype=torch.bfloat16, device=dev, row_stride=stride)
     batches = synth.seed_batches(sh.num_nodes, 1024, 42, device=dev)
     ex = Fused2HopStep(g, X, 1024, sh.k1, sh.k2, use_graph=not a.eager)
-    ex.set_grad_out(torch.randn((1024, sh.d_feat), device=dev))
+    ex.set_grad_out(torch.randn((1024, sh.d_feat), device=dev).to(X.dtype))
     flush = torch.ones(512 << 20 >> 3, dtype=torch.int64, device=dev)
     sink = torch.zeros(1, dtype=torch.int64, device=dev)
     for i in range(6):
@@ -46,17 +50,10 @@ def main():
     _lib.check(_lib.load().fsa_trace_geometry(_lib.C.byref(ns), _lib.C.byref(nb)), "geom")
     S, NB = ns.value, nb.value
     buf = torch.empty((S, NB, 2), dtype=torch.int64, device=dev)
-    if a.noatomic:
-        _lib.load().fsa_debug_noatomic(1)
     for rep in range(a.reps):
         buf[..., 0] = torch.iinfo(torch.int64).max
         buf[..., 1] = 0
         _lib.check(_lib.load().fsa_trace(buf.data_ptr()), "trace")
-        dbg = torch.zeros(64 * 8, dtype=torch.int64, device=dev)
-        L = _lib.load()
-        if hasattr(L, "fsa_debug"):
-            L.fsa_debug.argtypes = [_lib.C.c_void_p]
-            L.fsa_debug(dbg.data_ptr())
         torch.sum(flush, dim=0, keepdim=True, out=sink)
         torch.cuda.synchronize()
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
@@ -72,13 +69,6 @@ def main():
         cn = cnts.cpu().numpy()
         print(f"slots {s2.numel()} distinct {len(cn)} multi {int((cn > 1).sum())} big(>32) {int((cn > 32).sum())} "
               f"max count {int(cn.max())} top5 {sorted(cn.tolist())[-5:]}")
-        if hasattr(L, "fsa_debug"):
-            L.fsa_debug(None)
-            d = dbg.view(64, 8).cpu().numpy()
-            tt0 = t[..., 0][t[..., 1] > 0].min() if False else d[:, 0][d[:, 0] > 0].min()
-            for w in range(64):
-                if d[w, 0]:
-                    print("warp", w, [(int(x) - tt0) / 1e3 if x > 1e12 else int(x) for x in d[w]])
         used = t[..., 1] > 0
         t0 = t[..., 0][used].min()
         print(f"--- rep {rep}: step {ev[0].elapsed_time(ev[1]) * 1e3:.1f} us (events)")
