@@ -9,6 +9,8 @@ timeout 900 python -m pytest tests -m gpu -q > gpurun_out/${TAG}_pytest_gpu.log 
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1
 timeout 900 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
 timeout 300 python tools/timeline.py --reps 2 > gpurun_out/${TAG}_timeline.txt 2>&1
+timeout 300 python tools/timeline.py --config reddit --reps 1 > gpurun_out/${TAG}_timeline_reddit.txt 2>&1
+timeout 300 python tools/timeline.py --config arxiv --reps 1 > gpurun_out/${TAG}_timeline_arxiv.txt 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv \
     python tools/profile_step.py --alpha 3.0 --steps 3 > /dev/null 2>&1
 # one step = 6 forward + 8 backward launches (with the sparse re-zero); skip the first step
