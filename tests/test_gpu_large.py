@@ -1,0 +1,276 @@
+"""GPU parity at the benchmarked shapes (SURVEY.md §4.1 "large-shape parity"): the sm_100a path
+against the pinned CPU oracle on the BASELINE.json graphs, and on targeted graphs that drive the
+sampler through every code path the benchmarked shapes use.
+
+Reference behaviour matched: Algorithm R over ascending CSR rows (pkg/src/fsa/kernels.py:52-68)
+inside fused_2hop (kernels.py:152-198), the replay backward (fused.py:225-255, kernels.py:296-338).
+
+Gates: s1 / s2 bitwise; fp32 out and gradient bitwise (plus the 1e-5 relative gate); bf16 within
+1e-2 of the fp32 oracle on bf16-rounded inputs (and bitwise to its single rounding).  Each shape
+runs two batches through the per-call API (fused_2hop_forward / fused_2hop_backward) and two
+through the CUDA-graph step executor (executor.Fused2HopStep).
+
+Sampler paths and the cases that reach them (paper_2511_13645_b200/csrc/fsa_kernels.cu):
+  * short buckets, Barrett remainder (m < FAST_M = 16,384): every shape;
+  * fraction fast path (m >= FAST_M): hub rows of the alpha=2.1 shapes, ``test_fraction_path_hubs``;
+  * long buckets (SEG > 256 draws: the chunk loop with modulus re-staging): ``test_long_buckets``
+    (bucket divisor forced so that SEG reaches 4,096) and the alpha=2.1 products shape;
+  * moduli beyond the table (m >= 2^21, constants computed inline): ``test_star_beyond_table``;
+  * 64-bit remainder (m > 2^30): ``test_row_longer_than_2_pow_30``.
+"""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+FP32_RTOL = 1e-5
+BF16_RTOL = 1e-2
+SEED = 42
+
+
+@pytest.fixture(scope="module")
+def fsa():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2511_13645_b200 as m
+    from paper_2511_13645_b200 import _lib
+    _lib.load()
+    return m
+
+
+@pytest.fixture(scope="module")
+def oracle():
+    from oracle import oracle as o
+    o.load()
+    o.set_threads(os.cpu_count() or 1)
+    return o
+
+
+def _bytes_equal(got: torch.Tensor, want: np.ndarray) -> bool:
+    g = got.detach().cpu().numpy()
+    return g.shape == want.shape and g.dtype == want.dtype and g.tobytes() == want.tobytes()
+
+
+def _rel_close(got: torch.Tensor, want: np.ndarray, rtol: float) -> None:
+    g = got.detach().double().cpu().numpy()
+    w = want.astype(np.float64)
+    scale = max(1.0, float(np.abs(w).max(initial=0.0)))
+    err = float(np.abs(g - w).max(initial=0.0))
+    assert err <= rtol * scale, f"max abs err {err} > {rtol} * {scale}"
+
+
+class Case:
+    """One graph + features on the device, the same arrays on the host for the oracle."""
+
+    def __init__(self, fsa, g, X, k1, k2, name):
+        self.fsa, self.g, self.X, self.k1, self.k2, self.name = fsa, g, X, k1, k2, name
+        self.N, self.D = g.num_nodes, X.shape[1]
+        self.rp, self.col = g.cpu_arrays()
+        # the oracle computes in fp32 on exactly the values the kernel reads
+        self.Xh = X.float().contiguous().cpu().numpy()
+
+    def batches(self, B, n=2):
+        from paper_2511_13645_b200 import synth
+        it = synth.seed_batches(self.N, B, SEED, device=self.X.device)
+        return [next(it) for _ in range(n)]
+
+    def oracle_step(self, oracle, seeds, base_seed, gout, root_offset=0):
+        out, s1, s2, _, _ = oracle.fused_2hop(self.rp, self.col, self.Xh, seeds.cpu().numpy(), self.k1, self.k2,
+                                              base_seed, root_offset=root_offset)
+        grad = oracle.backward_2hop(gout.float().cpu().numpy(), s1, s2, self.N)
+        return out, s1, s2, grad
+
+    def check(self, oracle, got_out, got_s1, got_s2, got_grad, want, what):
+        out, s1, s2, grad = want
+        assert _bytes_equal(got_s1, s1), f"{self.name} {what}: s1 differs"
+        assert _bytes_equal(got_s2, s2), f"{self.name} {what}: s2 differs"
+        if self.X.dtype == torch.float32:
+            assert _bytes_equal(got_out, out), f"{self.name} {what}: out not bitwise"
+            _rel_close(got_out, out, FP32_RTOL)
+            assert _bytes_equal(got_grad, grad), f"{self.name} {what}: grad not bitwise"
+            _rel_close(got_grad, grad, FP32_RTOL)
+        else:  # fp32 accumulation, one rounding at the end
+            dt = self.X.dtype
+            assert torch.equal(got_out, torch.from_numpy(out).to(got_out.device).to(dt)), f"{self.name} {what}: out"
+            _rel_close(got_out, out, BF16_RTOL)
+            assert torch.equal(got_grad, torch.from_numpy(grad).to(got_grad.device).to(dt)), \
+                f"{self.name} {what}: grad"
+            _rel_close(got_grad, grad, BF16_RTOL)
+
+    def run_api(self, oracle, B=1024, n=2):
+        fsa = self.fsa
+        gbuf = torch.zeros((self.N, self.D), dtype=self.X.dtype, device=self.X.device)
+        gen = torch.Generator(device=self.X.device)
+        gen.manual_seed(7)
+        for i, seeds in enumerate(self.batches(B, n)):
+            bs = fsa.step_seed(SEED, i)
+            gout = torch.randn((B, self.D), generator=gen, device=self.X.device).to(self.X.dtype)
+            out, idx = fsa.fused_2hop_forward(self.g, self.X, seeds, self.k1, self.k2, bs)
+            grad = fsa.fused_2hop_backward(gout, idx, self.N, out=gbuf, zero="sparse")
+            self.check(oracle, out, idx.s1, idx.s2, grad, self.oracle_step(oracle, seeds, bs, gout), f"api batch {i}")
+
+    def run_executor(self, oracle, B=1024, n=2):
+        from paper_2511_13645_b200.executor import Fused2HopStep
+        fsa = self.fsa
+        ex = Fused2HopStep(self.g, self.X, B, self.k1, self.k2)
+        gen = torch.Generator(device=self.X.device)
+        gen.manual_seed(8)
+        batches = self.batches(B, n + 3)
+        # the first use of each parity runs eagerly, then each parity's graph is captured and
+        # replayed: check the eager steps and the replays
+        for i, seeds in enumerate(batches):
+            bs = fsa.step_seed(SEED + 1, i)
+            gout = torch.randn((B, self.D), generator=gen, device=self.X.device).to(self.X.dtype)
+            out, idx = ex.run(seeds, bs, gout)
+            torch.cuda.synchronize()
+            if i in (0, n + 1, n + 2):
+                self.check(oracle, out, idx.s1, idx.s2, ex.grad, self.oracle_step(oracle, seeds, bs, gout),
+                           f"executor step {i}")
+
+
+_CACHE: dict = {}
+
+
+def shape_case(fsa, config, alpha, dtype=torch.float32):
+    key = (config, alpha, dtype)
+    if key not in _CACHE:
+        _CACHE.clear()
+        torch.cuda.empty_cache()
+        from paper_2511_13645_b200 import synth
+        sh = synth.SHAPES[config]
+        g = synth.gen_power_law(sh.num_nodes, sh.avg_degree, alpha, SEED, device="cuda")
+        elem = 2 if dtype in (torch.bfloat16, torch.float16) else 4
+        stride = -(-sh.d_feat * elem // 16) * 16 // elem
+        X = synth.make_features(sh.num_nodes, sh.d_feat, SEED, dtype=dtype, device="cuda", row_stride=stride)
+        _CACHE[key] = Case(fsa, g, X, sh.k1, sh.k2, f"{config} alpha={alpha} {dtype}")
+    return _CACHE[key]
+
+
+# ---- BASELINE.json shapes ------------------------------------------------------------------------
+SHAPE_CASES = [
+    ("products", 3.0, torch.float32),
+    ("products", 2.1, torch.float32),
+    ("products25", 3.0, torch.float32),
+    ("reddit", 3.0, torch.float32),
+    ("reddit", 3.0, torch.bfloat16),
+    ("arxiv", 3.0, torch.float32),
+    ("arxiv", 2.1, torch.float32),
+]
+
+
+@pytest.mark.parametrize("config,alpha,dtype", SHAPE_CASES, ids=[f"{c}-a{a}-{str(d)[6:]}" for c, a, d in SHAPE_CASES])
+def test_benchmarked_shape_api(fsa, oracle, config, alpha, dtype):
+    shape_case(fsa, config, alpha, dtype).run_api(oracle)
+
+
+@pytest.mark.parametrize("config,alpha,dtype", SHAPE_CASES, ids=[f"{c}-a{a}-{str(d)[6:]}" for c, a, d in SHAPE_CASES])
+def test_benchmarked_shape_executor(fsa, oracle, config, alpha, dtype):
+    shape_case(fsa, config, alpha, dtype).run_executor(oracle)
+
+
+def test_sharded_products_equals_single_gpu(fsa, oracle):
+    """Seed sharding (root_offset = global position): two shards concatenated are bitwise the
+    1-GPU batch at the products shape."""
+    c = shape_case(fsa, "products", 3.0)
+    seeds = c.batches(1024, 1)[0]
+    bs = fsa.step_seed(SEED, 5)
+    out, idx = fsa.fused_2hop_forward(c.g, c.X, seeds, c.k1, c.k2, bs)
+    parts = [fsa.fused_2hop_forward(c.g, c.X, seeds[lo:hi], c.k1, c.k2, bs, root_offset=lo)
+             for lo, hi in ((0, 512), (512, 1024))]
+    assert torch.equal(torch.cat([p[0] for p in parts]), out)
+    assert torch.equal(torch.cat([p[1].s2 for p in parts]), idx.s2)
+    _, s1, s2, _, _ = oracle.fused_2hop(c.rp, c.col, c.Xh, seeds[512:].cpu().numpy(), c.k1, c.k2, bs, root_offset=512)
+    assert _bytes_equal(parts[1][1].s2, s2)
+
+
+# ---- targeted sampler paths ---------------------------------------------------------------------
+def _hub_graph(n_hubs, n_leaves, rng):
+    """Bipartite hubs x leaves (every leaf lists every hub): leaf rows have n_hubs neighbours,
+    hub rows n_leaves.  Nodes 0..n_hubs-1 are hubs."""
+    n = n_hubs + n_leaves
+    hub_row = np.arange(n_hubs, n, dtype=np.int32)
+    col = np.concatenate([np.tile(hub_row, n_hubs), np.tile(np.arange(n_hubs, dtype=np.int32), n_leaves)])
+    deg = np.concatenate([np.full(n_hubs, n_leaves), np.full(n_leaves, n_hubs)])
+    rowptr = np.zeros(n + 1, np.int64)
+    rowptr[1:] = np.cumsum(deg)
+    return rowptr, col, n
+
+
+def _custom_case(fsa, rowptr, col, n, D, k1, k2, name, validate=True, seed=3):
+    g = fsa.CsrGraph.from_arrays(rowptr, col, device="cuda", num_nodes=n, validate=validate)
+    X = torch.randn((n, D), generator=torch.Generator(device="cuda").manual_seed(seed), device="cuda")
+    return Case(fsa, g, X, k1, k2, name)
+
+
+def test_fraction_path_hubs(fsa, oracle):
+    """Every second-hop chain runs over a 120,000-neighbour row: draws with m = i + 1 from 11 to
+    120,000 cross FAST_M, so most of them take the division-free fraction test."""
+    rng = np.random.default_rng(1)
+    rowptr, col, n = _hub_graph(40, 120_000, rng)
+    c = _custom_case(fsa, rowptr, col, n, 32, 15, 10, "hubs 40 x 120k")
+    c.run_api(oracle, B=256, n=2)
+
+
+def test_long_buckets(fsa, oracle):
+    """Bucket divisor forced high (fsa_tune 1): the sampler picks SEG up to 4,096 draws per lane,
+    so the long-bucket chunk loop (modulus constants re-staged every 256 draws) runs at both
+    hops, on the hub graph (fraction path) and on the alpha=2.1 arxiv shape (Barrett path)."""
+    from paper_2511_13645_b200 import _lib
+    lib = _lib.load()
+    rng = np.random.default_rng(2)
+    rowptr, col, n = _hub_graph(24, 50_000, rng)
+    hub = _custom_case(fsa, rowptr, col, n, 16, 15, 10, "hubs 24 x 50k, long buckets")
+    try:
+        _lib.check(lib.fsa_tune(1, 1 << 20), "fsa_tune")
+        hub.run_api(oracle, B=512, n=1)
+        shape_case(fsa, "arxiv", 2.1).run_api(oracle, n=1)
+    finally:
+        _lib.check(lib.fsa_tune(1, 3), "fsa_tune")
+
+
+def test_star_beyond_table(fsa, oracle):
+    """A star with 2,300,000 leaves: the centre's chain runs moduli past RECIP_N = 2^21, whose
+    constants are computed inline.  Roots mix the centre (hop-1 chain of 2.3 M draws) and leaves
+    (whose single neighbour, the centre, gives hop-2 chains of 2.3 M draws)."""
+    leaves = 2_300_000
+    n = leaves + 1
+    rowptr = np.zeros(n + 1, np.int64)
+    rowptr[1] = leaves
+    rowptr[2:] = leaves + np.arange(1, leaves + 1)
+    col = np.concatenate([np.arange(1, n), np.zeros(leaves, np.int64)]).astype(np.int32)
+    c = _custom_case(fsa, rowptr, col, n, 8, 15, 10, "star 2.3M")
+    gen = torch.Generator(device="cuda").manual_seed(4)
+    seeds = torch.randint(1, n, (48,), generator=gen, device="cuda")
+    seeds[::6] = 0
+    bs = fsa.step_seed(SEED, 11)
+    gout = torch.randn((48, 8), generator=gen, device="cuda")
+    out, idx = fsa.fused_2hop_forward(c.g, c.X, seeds, c.k1, c.k2, bs)
+    grad = fsa.fused_2hop_backward(gout, idx, n)
+    c.check(oracle, out, idx.s1, idx.s2, grad, c.oracle_step(oracle, seeds, bs, gout), "star")
+
+
+def test_row_longer_than_2_pow_30(fsa, oracle):
+    """One row of 2^30 + 2^16 neighbours (ids cycling over 2^20 nodes; the operator does not need
+    distinct neighbours): draws with m > 2^30 take the 64-bit remainder path."""
+    E = (1 << 30) + (1 << 16)
+    nn = 1 << 20
+    n = nn + 1
+    try:
+        col_d = (torch.arange(E, device="cuda", dtype=torch.int64) % nn + 1).to(torch.int32)
+    except torch.OutOfMemoryError:
+        pytest.skip("device memory")
+    rowptr = np.zeros(n + 1, np.int64)
+    rowptr[1:] = E
+    g = fsa.CsrGraph(n, torch.from_numpy(rowptr.astype(np.int32)).cuda(), col_d)
+    seeds = torch.zeros(2, dtype=torch.int64, device="cuda")
+    bs = fsa.step_seed(SEED, 13)
+    s1, s2, t1, _ = fsa.sample_2hop(g, seeds, 15, 10, bs)
+    o1, o2, ot1, _ = oracle.sample_2hop(rowptr.astype(np.int32), col_d.cpu().numpy(), seeds.cpu().numpy(), 15, 10, bs)
+    assert _bytes_equal(s1, o1) and _bytes_equal(s2, o2)
+    assert np.array_equal(t1.cpu().numpy(), ot1)
