@@ -7,11 +7,15 @@ forward + replay backward on an ogbn-products-shaped synthetic power-law graph (
 
 A step = one forward (fused_2hop_forward, save_indices=True) + one replay backward
 (fused_2hop_backward into a persistent N x D gradient buffer, re-zeroed sparsely) over one
-batch of B=1024 seeds per GPU.  Multi-GPU: one process per GPU (torchrun), seeds sharded by
-global batch position (root_offset), graph + features replicated, no collective on the data
-path -> weak scaling.  Timing: W warm-up steps, then K steps each bracketed by CUDA events on
-the operator's stream, L2 flushed (512 MiB memset) before every step outside the events,
-barrier + synchronize around the timed region, max over ranks.
+batch of B=1024 seeds per GPU.  Multi-GPU: one process per GPU (``--gpus N`` re-launches itself
+under torch.distributed.run when WORLD_SIZE is unset), seeds sharded by global batch position
+(root_offset), graph + features replicated, no collective on the data path -> weak scaling
+(headline); strong scaling (global B=1024) and the config-5 training step (products 25-10, SAGE
+head, NCCL all-reduce of the head gradients captured in the step graph) are reported beside it.
+Timing: W warm-up steps, then K steps each bracketed by CUDA events on the operator's stream,
+L2 flushed (512 MiB read) before every step outside the events, barrier + synchronize around
+the timed region, max over ranks.  Before timing, two batches of the executor step (one eager,
+one CUDA-graph replay) are checked against the CPU oracle ("parity").
 
 Also reported (one JSON line on rank 0): e2e through the public API with pinned host inputs,
 the dominant kernel's roofline (library CUDA-event timing + algorithmic bytes), the CPU
@@ -53,6 +57,8 @@ def parse_args():
     p.add_argument("--no-alt", action="store_true", help="skip the alpha=2.1 side measurement")
     p.add_argument("--no-unfused", action="store_true", help="skip the unfused-comparator measurement")
     p.add_argument("--no-train", action="store_true", help="skip the SAGE training-step measurement")
+    p.add_argument("--no-parity", action="store_true", help="skip the oracle check of two batches")
+    p.add_argument("--no-strong", action="store_true", help="skip the strong-scaling (global B) measurement")
     p.add_argument("--cpu-seconds", type=float, default=10.0)
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--profile", action="store_true", help="print the per-kernel table to stderr")
@@ -129,10 +135,17 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def _capture_order(path):
+    """(round, session) of a profiles/rNN[sM]_ncu_traffic.json name, compared numerically."""
+    import re
+    m = re.match(r"r(\d+)(?:_?s(\d+))?_", path.name)
+    return (int(m.group(1)), int(m.group(2) or 0)) if m else (-1, -1)
+
+
 def ncu_traffic(kernel):
     """dram__bytes_read.sum + dram__bytes_write.sum of one launch of ``kernel`` from the latest
     committed ncu --set full capture summary (profiles/r*_ncu_traffic.json), or None."""
-    files = sorted((ROOT / "profiles").glob("r*_ncu_traffic.json"))
+    files = sorted((ROOT / "profiles").glob("r*_ncu_traffic.json"), key=_capture_order)
     if not files:
         return None, None
     try:
@@ -194,30 +207,42 @@ def kernel_alg_bytes(name, B, k1, k2, D, E, T1, T2, U2, singles):
 
 
 class Runner:
-    """One rank's fused 2-hop fwd+bwd step loop on its shard of the global batch."""
+    """One rank's fused 2-hop fwd+bwd step loop on its shard of the global batch.
 
-    def __init__(self, args, shape, alpha, device, world, rank):
+    ``mode`` "weak": ``args.batch`` seeds per rank (global batch = batch x world); "strong":
+    the global batch is ``args.batch`` and each rank takes its contiguous shard.  ``inputs``
+    (graph, X) reuses another runner's device inputs; ``k1`` overrides the shape's fanout."""
+
+    def __init__(self, args, shape, alpha, device, world, rank, mode="weak", inputs=None, k1=None):
         import torch
         import paper_2511_13645_b200 as fsa
         from paper_2511_13645_b200 import synth
+        from paper_2511_13645_b200.shard import shard_bounds
 
         self.torch, self.fsa = torch, fsa
         self.args, self.shape, self.alpha = args, shape, alpha
-        self.device, self.world, self.rank = device, world, rank
+        self.device, self.world, self.rank, self.mode = device, world, rank, mode
         dtype = torch.bfloat16 if (args.dtype == "bf16" or (args.dtype is None and args.config == "reddit")) \
             else torch.float32
         self.dtype = dtype
         self.E = 2 if dtype == torch.bfloat16 else 4
         t0 = time.time()
-        self.g, self.X = make_inputs(shape, alpha, args.seed, device, dtype)
+        self.g, self.X = inputs if inputs is not None else make_inputs(shape, alpha, args.seed, device, dtype)
         torch.cuda.synchronize(device)
         self.gen_s = time.time() - t0
         self.N, self.D = shape.num_nodes, shape.d_feat
-        self.B, self.k1, self.k2 = args.batch, shape.k1, shape.k2
-        self.root_offset = rank * self.B
+        self.k1, self.k2 = (k1 or shape.k1), shape.k2
+        if mode == "weak":
+            self.global_B = args.batch * world
+            lo, hi = rank * args.batch, (rank + 1) * args.batch
+        else:
+            self.global_B = args.batch
+            lo, hi = shard_bounds(args.batch, rank, world)
+        self.B, self.root_offset = hi - lo, lo
         nsteps = max(args.warmup + args.steps, 64) + 8  # the e2e / per-call legs cycle through them
-        gb = synth.seed_batches(self.N, self.B * world, args.seed, device=device)
-        self.batches = [next(gb)[self.root_offset:self.root_offset + self.B].contiguous() for _ in range(nsteps)]
+        gb = synth.seed_batches(self.N, self.global_B, args.seed, device=device)
+        self.global_batches = [next(gb) for _ in range(nsteps)]
+        self.batches = [b[lo:hi].contiguous() for b in self.global_batches]
         self.base_seeds = [fsa.step_seed(args.seed, i) for i in range(nsteps)]
         gen = torch.Generator(device=device)
         gen.manual_seed(args.seed + 7)
@@ -230,6 +255,45 @@ class Runner:
                                 use_graph=not args.eager)
         self.ex.set_grad_out(self.gout)
         self.idx = None
+
+    def parity(self, n_batches=2):
+        """The executor's step against the CPU oracle (test infrastructure, outside every timed
+        region) on this rank's shard: steps 0..3 run (the first use of each parity is eager, then
+        each parity's graph is captured and replayed), batches 0 (eager) and 3 (graph replay) are
+        compared: s1 / s2 bitwise, out and the feature gradient bitwise in fp32 (bf16: equal to
+        the single rounding of the fp32 oracle on the same bf16 inputs, within 1e-2)."""
+        torch = self.torch
+        from oracle import oracle
+        oracle.set_threads(os.cpu_count() or 1)
+        rp, col = self.g.cpu_arrays()
+        Xh = self.X.float().contiguous().cpu().numpy()
+        gh = self.gout.float().cpu().numpy()
+        checked, bitwise, worst = 0, True, 0.0
+        want_steps = {0, 3} if n_batches >= 2 else {0}
+        for i in range(4):
+            out, idx = self.ex.run(self.batches[i], self.base_seeds[i], self.gout)
+            if i not in want_steps:
+                continue
+            torch.cuda.synchronize(self.device)
+            o_out, s1, s2, _, _ = oracle.fused_2hop(rp, col, Xh, self.batches[i].cpu().numpy(), self.k1, self.k2,
+                                                    self.base_seeds[i], root_offset=self.root_offset)
+            o_grad = oracle.backward_2hop(gh, s1, s2, self.N)
+            ok_idx = np.array_equal(idx.s1.cpu().numpy(), s1) and np.array_equal(idx.s2.cpu().numpy(), s2)
+            if self.dtype == torch.float32:
+                ok_val = out.cpu().numpy().tobytes() == o_out.tobytes() and \
+                    self.ex.grad.cpu().numpy().tobytes() == o_grad.tobytes()
+            else:
+                ok_val = torch.equal(out, torch.from_numpy(o_out).to(self.device).to(self.dtype)) and \
+                    torch.equal(self.ex.grad, torch.from_numpy(o_grad).to(self.device).to(self.dtype))
+            for a, b in ((out, o_out), (self.ex.grad, o_grad)):
+                d = float((a.float() - torch.from_numpy(b).to(self.device)).abs().max())
+                worst = max(worst, d / max(1.0, float(np.abs(b).max())))
+            bitwise = bitwise and ok_idx and ok_val
+            checked += 1
+        torch.cuda.synchronize(self.device)
+        return {"checked_batches": checked, "bitwise": bool(bitwise), "max_rel_err": worst,
+                "what": "executor step (eager + CUDA-graph replay) vs the CPU oracle: s1/s2, out, feature grad",
+                "rank": self.rank, "root_offset": self.root_offset}
 
     def flush_l2(self):
         """Evict L2 (126 MB) before a timed step, outside its events: a 512 MiB read (default)
@@ -245,7 +309,7 @@ class Runner:
     def step(self, i):
         nb = len(self.batches)
         out, idx = self.ex.run(self.batches[i % nb], self.base_seeds[i % nb])
-        self.idx = idx
+        self.idx, self.last_i = idx, i % nb
         return out
 
     def eager_step(self, i):
@@ -307,7 +371,7 @@ class Runner:
         torch = self.torch
         rp = self.g.rowptr.to(torch.int64)
         deg = rp[1:] - rp[:-1]
-        seeds = self.batches[self.args.warmup + self.args.steps - 1]
+        seeds = self.batches[self.last_i]
         s1 = self.idx.s1[self.idx.s1 >= 0].to(torch.int64)
         return int((deg[seeds] - self.k1).clamp_min(0).sum() + (deg[s1] - self.k2).clamp_min(0).sum())
 
@@ -390,9 +454,10 @@ class Runner:
 
 
     def train(self, steps, warmup, graph_mode, hidden=256, classes=47):
-        """SAGE training step (SURVEY.md §8d config 4: head H=256, C=47, AdamW) around the fused
-        op: eager train_step, or GraphTrainStep (CUDA graphs).  Device-resident seeds/labels.
-        Returns ms per step."""
+        """SAGE training step (SURVEY.md §8d config 4/5: head H=256, C=47, AdamW) around the fused
+        op: GraphTrainStep (CUDA graphs; with world > 1 the head-gradient all-reduce is captured in
+        the step graph) or the eager train_step (handed the GLOBAL batch: it shards it itself and
+        all-reduces).  Device-resident seeds/labels.  Returns ms per step, max over ranks."""
         torch, fsa = self.torch, self.fsa
         from paper_2511_13645_b200 import train as tr
         state = tr.init_train_state(self.D, hidden, classes, 42, dtype=torch.float32, device=self.device)
@@ -401,20 +466,25 @@ class Runner:
         labels = torch.randint(0, classes, (self.N,), generator=gen, device=self.device)
         X = self.X
         if graph_mode:
-            gts = tr.GraphTrainStep(self.g, X, self.B, (self.k1, self.k2), state, root_offset=self.root_offset)
+            gts = tr.GraphTrainStep(self.g, X, self.B, (self.k1, self.k2), state, root_offset=self.root_offset,
+                                    global_batch=self.global_B)
         gbuf = torch.zeros((self.N, self.D), dtype=X.dtype, device=self.device)
+        nb = len(self.batches)
 
         def one(i):
-            seeds = self.batches[i % len(self.batches)]
+            j = i % nb
             if graph_mode:
-                gts.run(seeds, labels[seeds], self.base_seeds[i % len(self.base_seeds)])
+                gts.run(self.batches[j], labels[self.batches[j]], self.base_seeds[j])
             else:
-                tr.train_step(self.g, X, fsa.SeedBatch(seeds, labels[seeds]), (self.k1, self.k2),
-                              self.base_seeds[i % len(self.base_seeds)],
-                              "fused", state, grad_scratch=gbuf)
+                gseeds = self.global_batches[j]
+                tr.train_step(self.g, X, fsa.SeedBatch(gseeds, labels[gseeds]), (self.k1, self.k2),
+                              self.base_seeds[j], "fused", state, grad_scratch=gbuf)
 
         for i in range(warmup):
             one(i)
+        torch.cuda.synchronize(self.device)
+        if self.world > 1:
+            torch.distributed.barrier()
         torch.cuda.synchronize(self.device)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
@@ -422,7 +492,10 @@ class Runner:
             one(warmup + j)
         b.record()
         torch.cuda.synchronize(self.device)
-        return a.elapsed_time(b) / steps
+        ms = a.elapsed_time(b) / steps
+        if self.world > 1:
+            torch.distributed.barrier()
+        return max_over_ranks(ms, self.world, self.device)
 
     def per_call(self, steps, warmup, impl):
         """Device time of one fwd+bwd through the per-call API with device-resident inputs:
@@ -536,6 +609,11 @@ def run_fused(args):
 
     def measure(alpha, full=True):
         r = Runner(args, shape, alpha, device, world, rank)
+        parity = None
+        if full and rank == 0 and not args.no_parity:
+            parity = r.parity()
+        if world > 1:
+            torch.distributed.barrier()
         with ClockSampler(gpu) as clk:
             ms, launches, wall = r.timed(args.steps, args.warmup)
         mean_ms = statistics.mean(ms)
@@ -543,7 +621,7 @@ def run_fused(args):
         T1, T2, U2, singles = r.stats()
         res = {"runner": r, "ms": ms_max, "ms_local": mean_ms, "launches": launches, "clocks": clk.summary(),
                "T1": T1, "T2": T2, "U2": U2, "singles": singles, "draws": r.draws(), "gen_s": r.gen_s,
-               "p50": statistics.median(ms), "wall": wall}
+               "p50": statistics.median(ms), "wall": wall, "parity": parity}
         if full:
             res["prof"] = r.profile()
             res["e2e"] = r.e2e(max(20, args.steps // 2), 3)
@@ -557,6 +635,35 @@ def run_fused(args):
 
     main = measure(args.alpha)
     r = main["runner"]
+    strong = None
+    if world > 1 and not args.no_strong:  # the same op step with the global batch fixed at args.batch
+        rs = Runner(args, shape, args.alpha, device, world, rank, mode="strong", inputs=(r.g, r.X))
+        ms_s, _, _ = rs.timed(max(20, args.steps // 2), args.warmup)
+        ms_s = max_over_ranks(statistics.mean(ms_s), world, device)
+        strong = {"global_batch": rs.global_B, "batch_per_gpu": [rs.B, "rank 0"], "ms_per_step": round(ms_s, 5),
+                  "value": round(rs.global_B / (ms_s / 1e3), 1), "unit": "seeds/s"}
+        del rs
+    elif world == 1:
+        strong = {"global_batch": r.global_B, "batch_per_gpu": r.B, "ms_per_step": round(main["ms"], 5),
+                  "value": round(r.global_B / (main["ms"] / 1e3), 1), "unit": "seeds/s",
+                  "note": "N=1: the strong-scaling workload is the headline workload"}
+    config5 = None
+    if not args.no_train and args.config in ("products", "products25") and r.dtype == torch.float32:
+        # BASELINE.json config 5: products 25-10 SAGE training step, seed-sharded, NCCL all-reduce of
+        # the head gradients (captured in the step's CUDA graph); same graph and features
+        config5 = {"workload": "ogbn-products-shaped 2-hop (25,10) SAGE-mean training step (fused op fwd+bwd, "
+                               "head H=256 C=47, cross-entropy, AdamW), GraphTrainStep",
+                   "collective": "one all-reduce of the head gradients + loss per step (254 KB fp32), "
+                                 + ("NCCL, captured in the step graph" if world > 1 and backend == "nccl"
+                                    else "none at N=1" if world == 1 else f"{backend}, eager step"),
+                   "unit": "seeds/s"}
+        for mode in (("weak", "strong") if world > 1 else ("weak",)):
+            r5 = Runner(args, synth.SHAPES["products25"], args.alpha, device, world, rank, mode=mode,
+                        inputs=(r.g, r.X), k1=25)
+            ms5 = r5.train(max(20, args.steps // 4), 5, True)
+            config5[mode] = {"global_batch": r5.global_B, "ms_per_step": round(ms5, 5),
+                             "value": round(r5.global_B / (ms5 / 1e3), 1)}
+            del r5
     B, k1, k2, D, E = r.B, r.k1, r.k2, r.D, r.E
     fwd_b, bwd_b = alg_bytes(B, k1, k2, D, E, main["T1"], main["T2"], main["U2"])
     step_bytes = fwd_b + bwd_b
@@ -642,6 +749,12 @@ def run_fused(args):
                                  "path": "fused_2hop_forward + fused_2hop_backward(zero='sparse') per call"}},
         "p50_ms": round(main["p50"], 5),
     }
+    if main["parity"] is not None:
+        line["parity"] = main["parity"]
+    if strong is not None:
+        line["strong_scaling"] = strong
+    if config5 is not None:
+        line["config5_train"] = config5
     if "train" in main:  # the caller of the hot path: the SAGE training step around the fused op
         tr_ms = main["train"]
         line["train_step"] = {
@@ -735,8 +848,30 @@ def run_reference(args):
     print(json.dumps(line))
 
 
+def relaunch_ranks(args) -> int:
+    """``--gpus N`` (N > 1) without a torchrun environment: re-run this script as N ranks, one
+    process per GPU, under torch.distributed.run on 127.0.0.1; rank 0 prints the line."""
+    import socket
+    if os.environ.get("FSA_DIST_BACKEND", "nccl") == "nccl":
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} needs {args.gpus} GPUs, this node has {have} "
+                  "(FSA_DIST_BACKEND=gloo shares one GPU for a functional check)", file=sys.stderr)
+            return 2
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse_args()
+    if args.impl == "fused" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_ranks(args))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -196,5 +196,5 @@ def baseline_backward(grad_out, block: MaterializedBlock, num_nodes: int, out: O
                                              _index_tensor(block.take1, dev).data_ptr(), k, int(num_nodes),
                                              buf.data_ptr(), mode, d_gathered.data_ptr(), d_gathered.stride(0),
                                              ws.data_ptr(), ws.numel(), st), "fsa_baseline_1hop_bwd")
-    _remember_rows(out, zero, ids.reshape(-1))
+    _remember_rows(out, ids.reshape(-1))
     return buf

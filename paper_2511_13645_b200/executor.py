@@ -68,6 +68,10 @@ class Fused2HopStep:
         self.copy_out = torch.cuda.Stream(device=dev)  # device -> host outputs
         self.done = [torch.cuda.Event() for _ in range(2)]
         self.done_used = [False, False]
+        # D2H of a parity's out buffer finished: the next step of that parity (which rewrites
+        # out_p[p]) waits for it
+        self.out_copied = [torch.cuda.Event() for _ in range(2)]
+        self.out_copied_used = [False, False]
         self.s1 = torch.empty((B, k1), dtype=torch.int32, device=dev)
         self.s2 = [torch.full((B, k1, k2), -1, dtype=torch.int32, device=dev) for _ in range(2)]
         self.t1 = torch.empty(B, dtype=torch.int32, device=dev)
@@ -186,6 +190,9 @@ class Fused2HopStep:
                 self.grad_out_p[p].copy_(grad_out, non_blocking=True)
         b = int(base_seed) & 0xFFFFFFFFFFFFFFFF
         self.base_seed_p[p].fill_(b - (1 << 64) if b >= (1 << 63) else b)  # same 64 bits, int64 storage
+        if self.out_copied_used[p]:  # the previous D2H of out_p[p] must finish before it is rewritten
+            main.wait_event(self.out_copied[p])
+            self.out_copied_used[p] = False
         if self.use_graph:
             if self.steps_run < 2:  # first use of each parity runs eagerly (init, attributes)
                 self._launch(p)
@@ -201,6 +208,8 @@ class Fused2HopStep:
             self.copy_out.wait_event(self.done[p])
             with torch.cuda.stream(self.copy_out):
                 out_host.copy_(self.out_p[p], non_blocking=True)
+            self.out_copied[p].record(self.copy_out)
+            self.out_copied_used[p] = True
         self.steps_run += 1
         self.parity = 1 - p
         return self.out_p[p], SampledIndices2(self.s1, self.s2[p])

@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import ctypes as C
 import threading
+import weakref
 from dataclasses import dataclass
 from typing import Optional, Tuple, Union
 
@@ -328,7 +329,10 @@ def sample_2hop(graph, seeds, k1: int, k2: int, base_seed: int, *, root_offset: 
 # ---------------------------------------------------------------------------------------------
 # backward
 # ---------------------------------------------------------------------------------------------
-# buffer data_ptr -> (version after our write, ids whose rows we wrote)
+# id(buffer) -> (weakref to the buffer, its version after our write, data_ptr, shape, a private
+# copy of the ids whose rows we wrote).  The entry dies with the buffer, every backward that
+# writes the buffer (whatever its zero mode) replaces it, and a torch-side modification of the
+# buffer (version change) or a different tensor object forces a full fill.
 _SPARSE_STATE: dict = {}
 
 
@@ -369,12 +373,14 @@ def _grad_buffer(grad_out, num_nodes, out, zero, ids_flat):
             or not out.is_contiguous() or out.device != grad_out.device:
         raise ValueError("gradient buffer has wrong shape or dtype")
     if zero == "sparse":
-        prev = _SPARSE_STATE.get(out.data_ptr())
-        if prev is not None and prev[0] == out._version and prev[2] == tuple(out.shape):
-            rows = prev[1]
-            _lib.check(_lib.load().fsa_zero_rows(out.data_ptr(), out.shape[1], _DTYPE_CODE[out.dtype],
-                                                 rows.data_ptr(), rows.numel(), _stream(out.device)),
-                       "fsa_zero_rows")
+        prev = _SPARSE_STATE.get(id(out))
+        if prev is not None and prev[0]() is out and prev[1] == out._version and prev[2] == out.data_ptr() \
+                and prev[3] == tuple(out.shape):
+            rows = prev[4]
+            if rows.numel():
+                _lib.check(_lib.load().fsa_zero_rows(out.data_ptr(), out.shape[1], _DTYPE_CODE[out.dtype],
+                                                     rows.data_ptr(), rows.numel(), _stream(out.device)),
+                           "fsa_zero_rows")
             return out, 0
         return out, 1
     if zero != "full":
@@ -382,9 +388,14 @@ def _grad_buffer(grad_out, num_nodes, out, zero, ids_flat):
     return out, 1
 
 
-def _remember_rows(out, zero, ids_flat):
-    if out is not None and zero == "sparse":
-        _SPARSE_STATE[out.data_ptr()] = (out._version, ids_flat, tuple(out.shape))
+def _remember_rows(out, ids_flat):
+    """After a backward wrote ``out``: its nonzero rows are exactly the rows of ``ids_flat``."""
+    if out is None or not torch.is_tensor(out):
+        return
+    key = id(out)
+    rows = ids_flat.clone() if ids_flat is not None else torch.empty(0, dtype=torch.int32, device=out.device)
+    ref = weakref.ref(out, lambda _r, k=key: _SPARSE_STATE.pop(k, None))
+    _SPARSE_STATE[key] = (ref, out._version, out.data_ptr(), tuple(out.shape), rows)
 
 
 def fused_1hop_backward(grad_out, indices: Optional[SampledIndices1], num_nodes: int,
@@ -400,6 +411,7 @@ def fused_1hop_backward(grad_out, indices: Optional[SampledIndices1], num_nodes:
         buf, mode = _grad_buffer(g, num_nodes, out, "full", None)
         if mode == 1:
             buf.zero_()
+        _remember_rows(None if host_mode else out, None)
         return _host(buf) if host_mode else buf
     samples = _index_tensor(indices.samples, device)
     takes = _index_tensor(indices.takes, device)
@@ -420,7 +432,7 @@ def fused_1hop_backward(grad_out, indices: Optional[SampledIndices1], num_nodes:
         g.data_ptr(), B, g.shape[1], g.stride(0), _DTYPE_CODE[g.dtype], samples.data_ptr(),
         takes.data_ptr(), k, int(num_nodes), buf.data_ptr(), mode, None, None, None,
         ws.data_ptr(), ws.numel(), st), "fsa_fused_1hop_bwd")
-    _remember_rows(None if host_mode else out, zero, ids_flat)
+    _remember_rows(None if host_mode else out, ids_flat)
     if host_mode:
         res = _host(buf)
         if out is not None:
@@ -449,6 +461,7 @@ def fused_2hop_backward(grad_out, indices: Optional[SampledIndices2], num_nodes:
         buf, mode = _grad_buffer(g, num_nodes, out, "full", None)
         if mode == 1:
             buf.zero_()
+        _remember_rows(None if host_mode else out, None)
         return _host(buf) if host_mode else buf
     s1 = _index_tensor(indices.s1, device)
     s2 = _index_tensor(indices.s2, device)
@@ -470,7 +483,7 @@ def fused_2hop_backward(grad_out, indices: Optional[SampledIndices2], num_nodes:
         k1, k2, int(num_nodes), _ptr(buf), mode, _ptr(touched), _ptr(n_touched), _ptr(grad_rows),
         ws.data_ptr(), ws.numel(), st), "fsa_fused_2hop_bwd")
     if dense:
-        _remember_rows(None if host_mode else out, zero, ids_flat)
+        _remember_rows(None if host_mode else out, ids_flat)
     if host_mode and buf is not None:
         res = _host(buf)
         if out is not None and out is not False:

@@ -44,14 +44,16 @@ def shard_batch(seeds: torch.Tensor, rank: int, world: int) -> Tuple[torch.Tenso
 
 
 def allreduce_grads(grads: Dict[str, torch.Tensor], group=None, average: bool = True,
-                    flat: Optional[torch.Tensor] = None) -> Dict[str, torch.Tensor]:
+                    flat: Optional[torch.Tensor] = None, weight: Optional[float] = None) -> Dict[str, torch.Tensor]:
     """All-reduce a dict of gradients in ONE collective on a flattened buffer (in place).
 
-    ``average`` divides by the world size, turning per-rank batch means into the global-batch
-    mean (every rank holds the same number of seeds).  ``flat`` may supply a persistent buffer
-    of the total size (no allocation, CUDA-graph friendly)."""
+    ``weight`` (this rank's seeds / global seeds) scales each rank's batch means before the sum,
+    giving the global-batch mean also when shard sizes differ by one (shard_bounds); without it
+    ``average`` divides the sum by the world size (equal shards).  ``flat`` may supply a
+    persistent buffer of the total size (no allocation, CUDA-graph friendly).  With an explicit
+    ``weight`` the collective runs even in a world of one (a captured step keeps its shape)."""
     rank, world = dist_info(group)
-    if world == 1:
+    if world == 1 and weight is None:
         return grads
     names = list(grads)
     total = sum(grads[n].numel() for n in names)
@@ -63,8 +65,11 @@ def allreduce_grads(grads: Dict[str, torch.Tensor], group=None, average: bool = 
         k = grads[n].numel()
         flat[off:off + k].copy_(grads[n].reshape(-1))
         off += k
-    torch.distributed.all_reduce(flat, op=torch.distributed.ReduceOp.SUM, group=group)
-    if average:
+    if weight is not None:
+        flat.mul_(weight)
+    if world > 1 or torch.distributed.is_initialized():
+        torch.distributed.all_reduce(flat, op=torch.distributed.ReduceOp.SUM, group=group)
+    if weight is None and average:
         flat.div_(world)
     off = 0
     for n in names:
