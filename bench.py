@@ -54,6 +54,9 @@ def parse_args():
     p.add_argument("--batch", type=int, default=1024, help="seeds per GPU")
     p.add_argument("--dtype", default=None, choices=[None, "fp32", "bf16"])
     p.add_argument("--seed", type=int, default=42)
+    p.add_argument("--batch-stream", default="reference", choices=["reference", "device"],
+                   help="seed batches: the reference's numpy permutation stream (bench.py:172-179, bit-exact) "
+                        "or a torch device randperm")
     p.add_argument("--no-alt", action="store_true", help="skip the alpha=2.1 side measurement")
     p.add_argument("--no-unfused", action="store_true", help="skip the unfused-comparator measurement")
     p.add_argument("--no-train", action="store_true", help="skip the SAGE training-step measurement")
@@ -184,11 +187,9 @@ def make_inputs(shape, alpha, seed, device, dtype):
 
 
 def alg_bytes(B, k1, k2, D, E, T1, T2, U2):
-    """SURVEY.md §8d algorithmic bytes per batch (fwd, bwd)."""
-    idx = 4 * B * k1 * (1 + k2)
-    fwd = 8 * B + 8 * (B + T1) + 4 * (T1 + T2) + E * D * T2 + E * D * B + idx
-    bwd = E * D * B + idx + E * D * U2
-    return fwd, bwd
+    """SURVEY.md §8d algorithmic bytes per batch (fwd, bwd): paper_2511_13645_b200.metrics."""
+    from paper_2511_13645_b200.metrics import alg_bytes as ab
+    return ab(B, k1, k2, D, E, T1, T2, U2)
 
 
 def kernel_alg_bytes(name, B, k1, k2, D, E, T1, T2, U2, singles):
@@ -240,7 +241,8 @@ class Runner:
             lo, hi = shard_bounds(args.batch, rank, world)
         self.B, self.root_offset = hi - lo, lo
         nsteps = max(args.warmup + args.steps, 64) + 8  # the e2e / per-call legs cycle through them
-        gb = synth.seed_batches(self.N, self.global_B, args.seed, device=device)
+        stream = synth.reference_batches if args.batch_stream == "reference" else synth.seed_batches
+        gb = stream(self.N, self.global_B, args.seed, device=device)
         self.global_batches = [next(gb) for _ in range(nsteps)]
         self.batches = [b[lo:hi].contiguous() for b in self.global_batches]
         self.base_seeds = [fsa.step_seed(args.seed, i) for i in range(nsteps)]
@@ -572,6 +574,34 @@ def cpu_oracle_time(runner, budget_s, max_steps=None, threads=None):
     return times, threads
 
 
+def draw_peak(device):
+    """The sampler's integer roofline: whole-GPU draws/s of k_sample's draw loop in isolation
+    (fsa_bench_draws; tools/bench_draws.py), at the moduli the alpha=2.1 draws run at (the
+    fraction-test path, m >= 16,384), best of the one- and two-stream forms of the loop."""
+    import torch
+    from paper_2511_13645_b200 import _lib
+
+    lib = _lib.load()
+    sms = torch.cuda.get_device_properties(device).multi_processor_count
+    lanes, n = sms * 8 * 256, 4096
+    out = torch.zeros(2, dtype=torch.int64, device=device)
+    st = torch.cuda.current_stream(device)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    best = {}
+    for mode, name in ((1, "frac"), (3, "frac x2")):
+        ms = []
+        for _ in range(4):
+            a.record(st)
+            _lib.check(lib.fsa_bench_draws(mode, n, 200000, 15, lanes, out.data_ptr(), st.cuda_stream), "draws")
+            b.record(st)
+            torch.cuda.synchronize(device)
+            ms.append(a.elapsed_time(b))
+        best[name] = lanes * n / (min(ms[1:]) * 1e-3)
+    name = max(best, key=best.get)
+    return best[name], {"loop": name, "lanes": lanes, "draws_per_lane": n, "m0": 200000,
+                        "all": {k: round(v, 1) for k, v in best.items()}}
+
+
 def cpu_model():
     try:
         for ln in open("/proc/cpuinfo"):
@@ -713,7 +743,9 @@ def run_fused(args):
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "bf16" if r.dtype == torch.bfloat16 else "fp32",
-        "data": "synthetic (GPU power-law generator, graph.py:157 algorithm; standard-normal features)",
+        "data": "synthetic (GPU power-law generator, graph.py:157 algorithm; standard-normal features; seed "
+                + ("batches = the reference's _batch_stream, bench.py:172-179)" if args.batch_stream == "reference"
+                   else "batches from a device randperm)"),
         "config": {
             "workload": f"{shape.name} 2-hop ({k1},{k2}) fused sample+mean fwd+bwd, B={B}/GPU",
             "num_nodes": r.N, "arcs": r.g.num_edges, "max_degree": r.g.max_degree(), "alpha": args.alpha,
@@ -791,6 +823,20 @@ def run_fused(args):
                        "draws_per_s": round(alt["draws"] / (alt["ms"] / 1e3), 1),
                        "hbm_gbs": round((fb + bb) / (alt["ms"] / 1e3) / 1e9, 1),
                        "arcs": ra.g.num_edges, "max_degree": ra.g.max_degree(), "clocks": alt["clocks"]}
+        # second roofline: the sampler is integer-issue bound at alpha=2.1
+        aprof = ra.profile(steps=5)
+        samp = {k: v for k, v in aprof.items() if k.startswith("k_sample")}
+        samp_ms = sum(v[0] * v[1] for v in samp.values())
+        peak_d, peak_info = draw_peak(device)
+        ach_d = alt["draws"] / (samp_ms / 1e3) if samp_ms else None
+        line["alt"]["roofline"] = {
+            "bound": "int", "kernels": sorted(samp), "sampler_ms": round(samp_ms, 5),
+            "share_of_step": round(samp_ms / alt["ms_local"], 4),
+            "achieved_draws_s": round(ach_d, 1) if ach_d else None, "peak_draws_s": round(peak_d, 1),
+            "frac": round(ach_d / peak_d, 4) if ach_d else None, "unit": "draws/s",
+            "peak_kind": "measured: k_sample's draw loop on every resident warp (fsa_bench_draws)",
+            "peak_detail": peak_info,
+            "kernels_ms": {k: round(v[0], 5) for k, v in sorted(aprof.items())}}
         if rank == 0 and not args.no_cpu:
             times, threads = cpu_oracle_time(ra, args.cpu_seconds, max_steps=10)
             line["alt"]["cpu_baseline"] = {"value": round(B / statistics.median(times), 2), "unit": "seeds/s",
@@ -823,7 +869,8 @@ def run_reference(args):
     r.g, r.X = make_inputs(shape, args.alpha, args.seed, device, torch.float32)
     r.N, r.D, r.B, r.k1, r.k2 = shape.num_nodes, shape.d_feat, args.batch, shape.k1, shape.k2
     r.root_offset = 0
-    gb = synth.seed_batches(r.N, r.B, args.seed, device=device)
+    stream = synth.reference_batches if args.batch_stream == "reference" else synth.seed_batches
+    gb = stream(r.N, r.B, args.seed, device=device)
     r.batches = [next(gb) for _ in range(args.warmup + args.steps)]
     import paper_2511_13645_b200 as fsa
     r.base_seeds = [fsa.step_seed(args.seed, i) for i in range(len(r.batches))]

@@ -217,8 +217,11 @@ int fsa_jump(const uint64_t* states, const int64_t* dist, int64_t n, uint64_t* o
  * division differs bitwise from IEEE division: every divisor 1..dmax against every fp32
  * significand of two binades, plus sampled fp64 inputs. */
 int fsa_div_check(int dmax, unsigned long long* mismatches, void* stream);
-/* Micro-benchmark of the sampler's draw loop: one warp of `lanes` lanes, n draws per lane from
- * modulus m0 (mode 0 Barrett, 1 fraction test); out[0] = clock64 cycles, out[1] checksum. */
+/* Micro-benchmark of the sampler's draw loop: n draws per lane from modulus m0 (mode 0 Barrett,
+ * 1 fraction test, 2 / 3 the same as two interleaved streams per lane).  lanes <= 32: one warp,
+ * out[0] = clock64 cycles of lane 0; lanes > 32 (a multiple of 256): lanes / 256 CTAs of 256
+ * threads, for the caller to time with events (the GPU's draw throughput, the sampler roofline).
+ * n must be a multiple of 256. */
 int fsa_bench_draws(int mode, int n, uint32_t m0, int k, int lanes, unsigned long long* out, void* stream);
 /* ---- unfused comparator (baseline.py:63-194): the same sums with every intermediate in HBM ----
  * fsa_gather_rows: out[t] = X[ids[t]] (zero row for -1)                 (kernels.gather_rows)

@@ -115,3 +115,17 @@ def seed_batches(num_nodes: int, batch: int, seed: int, device="cuda"):
         perm = torch.randperm(num_nodes, generator=gen, device=device)
         for start in range(0, num_nodes - batch + 1, batch):
             yield perm[start:start + batch]
+
+
+def reference_batches(num_nodes: int, batch: int, base_seed: int, device="cuda"):
+    """The reference's own batch order, bit-exact (pkg/src/fsa/bench.py:172-179): numpy
+    ``default_rng([base_seed & 0xFFFFFFFF, 3]).permutation(num_nodes)`` per epoch, ragged tail
+    dropped.  The permutation is drawn on the host (numpy is the generator the contract names)
+    and uploaded once per epoch; batches are int64 device views of it."""
+    import numpy as np
+
+    rng = np.random.default_rng([base_seed & 0xFFFFFFFF, 3])
+    while True:
+        perm = torch.from_numpy(rng.permutation(num_nodes)).to(device)
+        for start in range(0, num_nodes - batch + 1, batch):
+            yield perm[start:start + batch]

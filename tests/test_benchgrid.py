@@ -40,6 +40,36 @@ def test_report_medians_and_ratios(tmp_path):
     assert list(got[0]) == bg.SUMMARY_COLUMNS and float(got[0]["mem_ratio"]) == 5.0
 
 
+def test_reference_schema_first_and_reference_files_read(tmp_path):
+    assert bg.CSV_COLUMNS[:len(bg.REF_COLUMNS)] == bg.REF_COLUMNS
+    assert bg.CSV_COLUMNS[len(bg.REF_COLUMNS):] == ["seeds_per_s", "hbm_gbs_alg", "frac_hbm_peak", "draws_per_s",
+                                                    "gpus", "alpha", "dtype", "cpu_cores"]
+    # a file written with the reference's columns only (its own harness) still parses
+    p = tmp_path / "ref.csv"
+    with open(p, "w", newline="") as fh:
+        w = csv.DictWriter(fh, fieldnames=bg.REF_COLUMNS)
+        w.writeheader()
+        for v in ("baseline", "fused"):
+            row = _rec(v, 0, 2.0 if v == "baseline" else 1.0, 10.0, 8).to_row()
+            w.writerow({c: row[c] for c in bg.REF_COLUMNS})
+    recs = bg.read_records(str(p))
+    assert [r.seeds_per_s for r in recs] == [None, None]
+    (s,) = bg.report_speedups(str(p))
+    assert s["step_speedup"] == 2.0 and s["fused_hbm_gbs_alg"] is None
+
+
+def test_extra_columns_round_trip(tmp_path):
+    r = _rec("fused", 0, 1.0, 5.0, 3)
+    r.seeds_per_s, r.hbm_gbs_alg, r.frac_hbm_peak, r.draws_per_s = 1024.0, 900.5, 0.14, 3.5e10
+    r.gpus, r.alpha, r.dtype, r.cpu_cores = 1, 2.1, "fp32", 16
+    p = tmp_path / "g.csv"
+    _rows(p, [r.to_row()])
+    (back,) = bg.read_records(str(p))
+    assert back.key() == r.key()
+    assert (back.seeds_per_s, back.hbm_gbs_alg, back.frac_hbm_peak, back.draws_per_s) == (1024.0, 900.5, 0.14, 3.5e10)
+    assert (back.gpus, back.alpha, back.dtype, back.cpu_cores) == (1, 2.1, "fp32", 16)
+
+
 def test_schema_errors(tmp_path):
     p = tmp_path / "bad.csv"
     p.write_text("dataset,variant\nx,fused\n")
@@ -72,3 +102,6 @@ def test_tiny_grid_on_the_gpu(tmp_path):
     (s,) = bg.report_speedups(str(out))
     assert s["fused_step_ms"] > 0 and s["baseline_step_ms"] > 0
     assert s["baseline_peak_bytes"] > s["fused_peak_bytes"]  # the materialised blocks
+    fused = [r for r in bg.read_records(str(out)) if r.config.variant == "fused"][0]
+    assert fused.seeds_per_s > 0 and fused.hbm_gbs_alg > 0 and 0 < fused.frac_hbm_peak < 1
+    assert fused.draws_per_s > 0 and fused.gpus == 1 and fused.alpha == 2.1 and fused.dtype == "fp32"

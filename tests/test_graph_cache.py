@@ -77,3 +77,18 @@ def test_interoperates_with_the_reference_writer_and_reader(tmp_path):
     assert p1.read_bytes() == p2.read_bytes()
     back = rg.load_csr_cache(p2)
     assert np.array_equal(back.col, ref.col)
+
+
+def test_reference_batch_stream_bitwise(reference_fsa):
+    """synth.reference_batches reproduces the reference's _batch_stream (bench.py:172-179),
+    including the reshuffle at the epoch boundary."""
+    import itertools
+
+    from fsa import bench as ref_bench
+    from paper_2511_13645_b200 import synth
+
+    for n, b, seed in ((1000, 96, 42), (2_449_029, 1024, 43)):
+        steps = n // b + 2 if n < 10_000 else 3
+        want = list(itertools.islice(ref_bench._batch_stream(n, b, seed), steps))
+        got = list(itertools.islice(synth.reference_batches(n, b, seed, device="cpu"), steps))
+        assert all(np.array_equal(w, g.numpy()) for w, g in zip(want, got))
