@@ -18,7 +18,7 @@ import torch
 
 from .graph import CsrGraph
 
-__all__ = ["SHAPES", "GraphShape", "gen_power_law", "make_features", "seed_batches"]
+__all__ = ["SHAPES", "GraphShape", "gen_power_law", "make_features", "seed_batches", "reference_batches"]
 
 
 @dataclass(frozen=True)

@@ -1,0 +1,18 @@
+#!/bin/bash
+# compute-sanitizer gate: memcheck, racecheck (shared-memory hazards), synccheck
+# and initcheck over smoke() and the small golden parity cases.  Logs: gpurun_out/${TAG}_sanitize_*.log
+mkdir -p gpurun_out
+TAG=${TAG:-r02}
+CS="compute-sanitizer --print-limit 50 --error-exitcode 99"
+SMOKE="python -c 'import __graft_entry__ as g; g.smoke()'"
+GOLD="python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k 'golden_cases or config1 or hub or wide or half or padded or sparse'"
+for tool in memcheck racecheck synccheck initcheck; do
+  log=gpurun_out/${TAG}_sanitize_${tool}.log
+  : > $log
+  for cmd in "$SMOKE" "$GOLD"; do
+    echo "### $tool: $cmd" >> $log
+    eval timeout 1500 $CS --tool $tool $cmd >> $log 2>&1
+    echo "### exit=$?" >> $log
+  done
+done
+grep -H "ERROR SUMMARY\|### exit" gpurun_out/${TAG}_sanitize_*.log
