@@ -6,6 +6,7 @@ There is no fallback: if the shared object is missing or fails to load, every op
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 from ._build import LIB_PATH
@@ -87,7 +88,8 @@ def load(path: Path | None = None) -> C.CDLL:
     global _LIB
     if _LIB is not None and path is None:
         return _LIB
-    p = Path(path) if path is not None else LIB_PATH
+    # FSA_LIB: an alternative build of the same ABI (A/B experiments, instrumented builds)
+    p = Path(path) if path is not None else Path(os.environ.get("FSA_LIB") or LIB_PATH)
     if not p.exists():
         raise ImportError(
             f"{p} is not built: run `python -c 'import __graft_entry__ as g; g.build()'` "

@@ -248,7 +248,7 @@ class Fused2HopStep:
 
     TRACE_NAMES = ("k_plan_roots", "k_sample1", "k_plan_hop2", "k_sample2", "k_gather2", "k_zero_rows",
                    "k_bwd_count", "k_bwd_single", "k_bwd_scatter", "k_bwd_multi", "k_bwd_big", "k_bwd_reserve",
-                   "k_final2", "k_bwd_terms")
+                   "k_final2", "k_bwd_terms", "k_hop1")
 
     def kernel_spans(self, seeds_list, base_seeds, flush=None) -> dict:
         """Per-kernel device time of the normal step graph, from the library's per-block

@@ -19,7 +19,7 @@ from paper_2511_13645_b200 import _lib, synth  # noqa: E402
 from paper_2511_13645_b200.executor import Fused2HopStep  # noqa: E402
 
 NAMES = ["plan_roots", "sample1", "plan_hop2", "sample2", "gather", "zero_rows", "bwd_count", "bwd_single",
-         "bwd_scatter", "bwd_multi", "bwd_big", "bwd_reserve", "final2", "bwd_terms"]
+         "bwd_scatter", "bwd_multi", "bwd_big", "bwd_reserve", "final2", "bwd_terms", "hop1"]
 
 
 def main():
