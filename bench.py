@@ -314,6 +314,18 @@ class Runner:
         self.idx, self.last_i = idx, i % nb
         return out
 
+    def stage(self, i):
+        """Step i's inputs (device-resident batch, base seed) into the executor's buffers, on its
+        copy stream; ``launch`` then runs the step."""
+        nb = len(self.batches)
+        self.ex.stage(self.batches[i % nb], self.base_seeds[i % nb])
+        self.last_i = i % nb
+
+    def launch(self):
+        out, idx = self.ex.launch()
+        self.idx = idx
+        return out
+
     def eager_step(self, i):
         """The same step through the public operator API (per-kernel profiling, launch counts)."""
         fsa = self.fsa
@@ -342,12 +354,20 @@ class Runner:
             torch.distributed.barrier()
         torch.cuda.synchronize(self.device)
         t_wall = time.perf_counter()
+        # The host enqueues a chunk of steps while the stream is parked behind a spin kernel, so
+        # each step's events time the device only: without it, the ~0.1 ms per step the host
+        # needs to submit a step (flush, input copies, graph launch) shows up inside the events
+        # whenever the device runs ahead of it.  The spin is outside every step's events.
+        chunk = 50
         for j in range(steps):
+            if j % chunk == 0:
+                torch.cuda._sleep(40_000_000)  # ~20 ms at 1.9 GHz: more than a chunk's host time
+            self.stage(warmup + j)  # inputs resident before the step's events (copy stream)
             if flush:
                 self.flush_l2()
             a, b = evs[j]
             a.record()
-            self.step(warmup + j)
+            self.launch()
             b.record()
         torch.cuda.synchronize(self.device)
         wall = time.perf_counter() - t_wall
@@ -615,7 +635,8 @@ def cpu_model():
 # ----------------------------------------------------------------------------------------------
 def run_fused(args):
     import torch
-    for knob, env in ((1, "FSA_SEG_DIV"), (2, "FSA_GATHER_PREFETCH"), (3, "FSA_ZERO_CTAS"), (4, "FSA_COUNT_CTAS"), (5, "FSA_MULTI_CTAS")):  # experiment knobs (fsa_tune)
+    for knob, env in ((1, "FSA_SEG_DIV"), (2, "FSA_GATHER_PREFETCH"), (3, "FSA_ZERO_CTAS"), (4, "FSA_COUNT_CTAS"),
+                      (5, "FSA_MULTI_CTAS"), (6, "FSA_HOP1")):  # experiment knobs (fsa_tune)
         if os.environ.get(env):
             from paper_2511_13645_b200 import _lib
             _lib.check(_lib.load().fsa_tune(knob, int(os.environ[env])), env)
@@ -755,6 +776,9 @@ def run_fused(args):
                            "(evicts L2, leaves it clean); inputs (1.5 GB CSR + features) are larger than L2",
                    "write": "flushed before every timed step by a 512 MiB write outside the step's CUDA events",
                    "none": "no flush; inputs (1.5 GB CSR + features, random rows) are larger than L2"}[args.flush],
+            "step_timing": "CUDA events around each step on its stream; the step's inputs are staged into the "
+                           "executor's buffers (copy stream) before its events; the host enqueues 50 steps at a "
+                           "time behind a spin kernel, so the events time device work, not host submission",
             "grad_buffer": "persistent N x D, sparse re-zero of the previous step's rows (fsa_zero_rows) "
                            "on a side stream overlapped with the forward",
             "execution": "eager" if args.eager else "CUDA graph per step (executor.Fused2HopStep)",

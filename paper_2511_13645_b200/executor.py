@@ -29,7 +29,7 @@ from typing import Optional
 import torch
 
 from . import _lib
-from .fused import _DTYPE_CODE, _set_device, SampledIndices2
+from .fused import _DTYPE_CODE, _select_hop1, _set_device, SampledIndices2
 from .graph import CsrGraph
 
 __all__ = ["Fused2HopStep"]
@@ -68,6 +68,7 @@ class Fused2HopStep:
         self.copy_out = torch.cuda.Stream(device=dev)  # device -> host outputs
         self.done = [torch.cuda.Event() for _ in range(2)]
         self.done_used = [False, False]
+        self.staged = False
         # D2H of a parity's out buffer finished: the next step of that parity (which rewrites
         # out_p[p]) waits for it
         self.out_copied = [torch.cuda.Event() for _ in range(2)]
@@ -116,6 +117,7 @@ class Fused2HopStep:
         bwd_args = (grad_out.data_ptr(), self.B, self.D, grad_out.stride(0), self.code,
                     self.s1.data_ptr(), cur.data_ptr(), self.k1, self.k2, self.N, self.grad.data_ptr(), 0, None,
                     None, None, self.ws_b.data_ptr(), self.ws_b.numel())
+        _select_hop1(self.g)  # baked into the captured graph
         _lib.check(lib.fsa_fused_2hop_fwd_phase(*fwd_args, _lib.FSA_FWD_SAMPLE), "fwd SAMPLE")
         if not self.overlap_zero:
             _lib.check(lib.fsa_fused_2hop_bwd_phase(*bwd_args, st, _lib.FSA_BWD_PLAN), "bwd PLAN")
@@ -171,25 +173,46 @@ class Fused2HopStep:
         step's output is copied back on the copy stream after the step.  ``grad_out=None`` reuses
         the content of this parity's buffer (see set_grad_out).  Returns
         ``(out, SampledIndices2)`` views of static buffers, valid until the step after next."""
+        if not self.staged:
+            self.stage(seeds, base_seed, grad_out)
+        elif seeds is not None or grad_out is not None:
+            raise ValueError("inputs were staged already: call run(None, base_seed)")
+        return self.launch(out_host)
+
+    def stage(self, seeds: Optional[torch.Tensor], base_seed: int, grad_out: Optional[torch.Tensor] = None) -> None:
+        """Copy the next step's inputs into its buffers on the copy stream (host or device
+        tensors), which waits only for the step that last read those buffers and for work queued
+        on the caller's stream when an input is a device tensor.  ``run`` does this itself;
+        calling it ahead of ``launch`` lets the copies overlap whatever the caller queues in
+        between."""
+        if self.staged:
+            raise ValueError("a staged step has not been launched yet")
         p = self.parity
         main = torch.cuda.current_stream(self.device)
-        host_in = (seeds is not None and not seeds.is_cuda) or (grad_out is not None and not grad_out.is_cuda)
-        if host_in:
-            if self.done_used[p]:
-                self.copy.wait_event(self.done[p])  # the step that last read these buffers is done
-            with torch.cuda.stream(self.copy):
-                if seeds is not None:
-                    self.seeds_p[p].copy_(seeds, non_blocking=True)
-                if grad_out is not None:
-                    self.grad_out_p[p].copy_(grad_out, non_blocking=True)
-            main.wait_stream(self.copy)
-        else:
+        if self.done_used[p]:
+            self.copy.wait_event(self.done[p])
+        dev_in = [t for t in (seeds, grad_out) if t is not None and t.is_cuda]
+        if dev_in:  # device inputs may come from work on the caller's stream
+            self.copy.wait_stream(main)
+        b = int(base_seed) & 0xFFFFFFFFFFFFFFFF
+        with torch.cuda.stream(self.copy):
             if seeds is not None:
                 self.seeds_p[p].copy_(seeds, non_blocking=True)
             if grad_out is not None:
                 self.grad_out_p[p].copy_(grad_out, non_blocking=True)
-        b = int(base_seed) & 0xFFFFFFFFFFFFFFFF
-        self.base_seed_p[p].fill_(b - (1 << 64) if b >= (1 << 63) else b)  # same 64 bits, int64 storage
+            self.base_seed_p[p].fill_(b - (1 << 64) if b >= (1 << 63) else b)  # same 64 bits, int64 storage
+        for t in dev_in:  # the caller may free them while the copy is pending
+            t.record_stream(self.copy)
+        self.staged = True
+
+    def launch(self, out_host: Optional[torch.Tensor] = None):
+        """Run the staged step on the current stream (see ``run``)."""
+        if not self.staged:
+            raise ValueError("no staged inputs: call stage() first (or run())")
+        self.staged = False
+        p = self.parity
+        main = torch.cuda.current_stream(self.device)
+        main.wait_stream(self.copy)
         if self.out_copied_used[p]:  # the previous D2H of out_p[p] must finish before it is rewritten
             main.wait_event(self.out_copied[p])
             self.out_copied_used[p] = False

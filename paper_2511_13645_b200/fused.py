@@ -22,6 +22,7 @@ Extensions over the reference, all optional keyword arguments:
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 import weakref
 from dataclasses import dataclass
@@ -116,6 +117,23 @@ def _ws(op: int, B: int, k1: int, k2: int, N: int, device: torch.device, stream:
         buf = torch.zeros(max(need, 1 << 20), dtype=torch.uint8, device=device)
         cache[key] = buf
     return buf
+
+
+# First-hop path of the 2-hop forward (fsa_tune 6): one warp per root (k_hop1) wins while first-hop
+# chains are short; the tile sampler wins on dense graphs (measured: products mean degree 50 and
+# arxiv 14 -> warp per root, 3 % / 5 % faster; Reddit 492 -> tiles, 7 % faster).  Both are
+# bitwise identical; FSA_HOP1 (1 / 2) pins the path for experiments.
+HOP1_TILE_MEAN_DEGREE = 128.0
+_hop1_set = [None]
+
+
+def _select_hop1(g) -> None:
+    if os.environ.get("FSA_HOP1"):
+        return
+    mode = 2 if g.num_edges > HOP1_TILE_MEAN_DEGREE * max(1, g.num_nodes) else 1
+    if _hop1_set[0] != mode:
+        _lib.check(_lib.load().fsa_tune(6, mode), "fsa_tune")
+        _hop1_set[0] = mode
 
 
 def _stream(device: torch.device) -> int:
@@ -266,6 +284,7 @@ def fused_2hop_forward(graph, X, roots, k1: int, k2: int, base_seed: int, save_i
     st = _stream(device)
     ws = _ws(_lib.FSA_OP_FWD2, B, k1, k2, 0, device, st)
     lib = _lib.load()
+    _select_hop1(g)
     _lib.check(lib.fsa_fused_2hop_fwd(
         g.rowptr.data_ptr(), g.col.data_ptr(), g.num_nodes, Xd.data_ptr(), D, Xd.stride(0),
         _DTYPE_CODE[Xd.dtype], sd.data_ptr(), B, int(root_offset), int(k1), int(k2),
@@ -318,6 +337,7 @@ def sample_2hop(graph, seeds, k1: int, k2: int, base_seed: int, *, root_offset: 
     _set_device(dev)
     st = _stream(dev)
     ws = _ws(_lib.FSA_OP_FWD2, B, k1, k2, 0, dev, st)
+    _select_hop1(g)
     _lib.check(_lib.load().fsa_fused_2hop_fwd(
         g.rowptr.data_ptr(), g.col.data_ptr(), g.num_nodes, None, 0, 0, _lib.FSA_F32,
         sd.data_ptr(), B, int(root_offset), int(k1), int(k2), _seed_u64(base_seed), 1,

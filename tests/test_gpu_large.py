@@ -234,6 +234,58 @@ def test_long_buckets(fsa, oracle):
         _lib.check(lib.fsa_tune(1, 3), "fsa_tune")
 
 
+@pytest.fixture
+def hop1_path():
+    """Pin the 2-hop forward's first-hop path (fsa_tune 6) for one test, then restore auto."""
+    from paper_2511_13645_b200 import _lib, fused
+    lib = _lib.load()
+    old = os.environ.get("FSA_HOP1")
+
+    def pin(mode):
+        os.environ["FSA_HOP1"] = str(mode)  # the operator then leaves the knob alone
+        _lib.check(lib.fsa_tune(6, mode), "fsa_tune")
+
+    yield pin
+    if old is None:
+        os.environ.pop("FSA_HOP1", None)
+    else:
+        os.environ["FSA_HOP1"] = old
+    fused._hop1_set[0] = None  # re-derive the automatic choice on the next call
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("config,alpha", [("products", 2.1), ("reddit", 3.0), ("arxiv", 3.0)])
+def test_first_hop_paths(fsa, oracle, hop1_path, mode, config, alpha):
+    """Both first-hop paths, whatever the graph would pick by default: one warp per root sampling,
+    finalising and planning its chain (k_hop1; chains longer than 8,192 draws split into queued
+    pieces), and the tile sampler with separate planning passes."""
+    hop1_path(mode)
+    c = shape_case(fsa, config, alpha)
+    c.run_api(oracle, n=1)
+    c.run_executor(oracle, n=1)
+
+
+def test_first_hop_piece_queue(fsa, oracle, hop1_path):
+    """k_hop1 with roots whose first-hop chains span many pieces (hubs of 120,000 neighbours):
+    pieces go through the device queue, winners through global atomics, and the warp that
+    finishes a root's last piece finalises it."""
+    hop1_path(1)
+    rng = np.random.default_rng(5)
+    rowptr, col, n = _hub_graph(40, 120_000, rng)
+    c = _custom_case(fsa, rowptr, col, n, 16, 15, 10, "hubs 40 x 120k, hub roots")
+    gen = torch.Generator(device="cuda").manual_seed(6)
+    # batch sizes change the workspace layout between calls: queue slots then hold other data
+    # (the tagged items must not be confused with it)
+    for i, B in enumerate((1024, 256, 64)):
+        seeds = torch.randint(0, n, (B,), generator=gen, device="cuda")
+        seeds[::3] = torch.randint(0, 40, (seeds[::3].numel(),), generator=gen, device="cuda")  # hub roots
+        bs = fsa.step_seed(SEED, 17 + i)
+        gout = torch.randn((B, 16), generator=gen, device="cuda")
+        out, idx = fsa.fused_2hop_forward(c.g, c.X, seeds, c.k1, c.k2, bs)
+        grad = fsa.fused_2hop_backward(gout, idx, n)
+        c.check(oracle, out, idx.s1, idx.s2, grad, c.oracle_step(oracle, seeds, bs, gout), f"hub roots B={B}")
+
+
 def test_star_beyond_table(fsa, oracle):
     """A star with 2,300,000 leaves: the centre's chain runs moduli past RECIP_N = 2^21, whose
     constants are computed inline.  Roots mix the centre (hop-1 chain of 2.3 M draws) and leaves
