@@ -202,10 +202,24 @@ int fsa_fused_2hop_bwd_phase(const void* grad_out, int64_t B, int64_t D, int64_t
                              int32_t* touched, int32_t* n_touched, void* grad_rows,
                              void* ws, size_t ws_bytes, void* stream, int phase);
 
+/* fsa_fused_2hop_bwd_phase into a dense gradient with row stride gx_stride (elements, >= D) of
+ * which the op may write the first gx_cols columns (D <= gx_cols <= gx_stride).  When gx_cols
+ * reaches D rounded up to 64 bytes, the row writers store whole 64-byte bursts (the padding
+ * columns get zeros): a persistent, op-owned buffer of padded rows is then written without
+ * partial bursts (400-byte fp32 rows, 1,204-byte bf16 rows).  No COO output. */
+int fsa_fused_2hop_bwd_phase_rows(const void* grad_out, int64_t B, int64_t D, int64_t g_stride, int dtype,
+                                  const int32_t* s1, const int32_t* s2, int32_t k1, int32_t k2, int64_t N,
+                                  void* grad_x, int64_t gx_stride, int64_t gx_cols, int zero_mode,
+                                  void* ws, size_t ws_bytes, void* stream, int phase);
+
 /* grad[rows[i], :] = 0 for i < n_rows, rows[i] < 0 skipped (duplicates harmless): sparse
  * re-zero of a persistent gradient buffer between steps, e.g. with the previous step's flat
  * s2 / samples as `rows`. */
 int fsa_zero_rows(void* grad, int64_t D, int dtype, const int32_t* rows, int64_t n_rows, void* stream);
+/* The same for rows of stride gx_stride, writing the first gx_cols columns (whole 64-byte bursts
+ * when gx_cols reaches D rounded up to 64 bytes, as fsa_fused_2hop_bwd_phase_rows). */
+int fsa_zero_rows_strided(void* grad, int64_t D, int64_t gx_stride, int64_t gx_cols, int dtype,
+                          const int32_t* rows, int64_t n_rows, void* stream);
 
 /* ---- test hooks (device arrays of length n) ---------------------------------------------- */
 int fsa_derive_states(const uint64_t* base_seed, const int64_t* root, const int64_t* hop,

@@ -58,6 +58,9 @@ SIGNATURES = {
     "fsa_fused_2hop_bwd_phase": (_int, [_p, _i64, _i64, _i64, _int, _p, _p, _i32, _i32, _i64, _p, _int, _p,
                                         _p, _p, _p, _sz, _p, _int]),
     "fsa_zero_rows": (_int, [_p, _i64, _int, _p, _i64, _p]),
+    "fsa_zero_rows_strided": (_int, [_p, _i64, _i64, _i64, _int, _p, _i64, _p]),
+    "fsa_fused_2hop_bwd_phase_rows": (_int, [_p, _i64, _i64, _i64, _int, _p, _p, _i32, _i32, _i64, _p, _i64, _i64,
+                                             _int, _p, _sz, _p, _int]),
     "fsa_derive_states": (_int, [_p, _p, _p, _p, _i64, _p, _p]),
     "fsa_xorshift_steps": (_int, [_u64, _i64, _p, _p]),
     "fsa_jump": (_int, [_p, _p, _i64, _p, _p]),

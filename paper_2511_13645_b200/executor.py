@@ -77,7 +77,12 @@ class Fused2HopStep:
         self.s2 = [torch.full((B, k1, k2), -1, dtype=torch.int32, device=dev) for _ in range(2)]
         self.t1 = torch.empty(B, dtype=torch.int32, device=dev)
         self.t2 = torch.empty((B, k1), dtype=torch.int32, device=dev)
-        self.grad = torch.zeros((N, D), dtype=self.dtype, device=dev)
+        # persistent feature gradient, rows padded to whole 64-byte bursts: the row writers and the
+        # re-zero store full bursts (no partial-burst read-modify-write); ``grad`` is the [N, D] view
+        e = torch.empty((), dtype=self.dtype).element_size()
+        self.gx_stride = -(-D * e // 64) * 64 // e
+        self.grad_full = torch.zeros((N, self.gx_stride), dtype=self.dtype, device=dev)
+        self.grad = self.grad_full[:, :D]
         self.ws_f = torch.zeros(lib.fsa_ws_bytes(_lib.FSA_OP_FWD2, B, k1, k2, 0, 0, 0), dtype=torch.uint8, device=dev)
         self.ws_b = torch.zeros(lib.fsa_ws_bytes(_lib.FSA_OP_BWD2, B, k1, k2, D, self.code, N), dtype=torch.uint8, device=dev)
         self.side = torch.cuda.Stream(device=dev)
@@ -106,8 +111,9 @@ class Fused2HopStep:
         if self.overlap_zero:
             zs.wait_stream(main)
         with torch.cuda.stream(zs):
-            _lib.check(lib.fsa_zero_rows(self.grad.data_ptr(), self.D, self.code, prev.data_ptr(), prev.numel(),
-                                         zs.cuda_stream), "fsa_zero_rows")
+            _lib.check(lib.fsa_zero_rows_strided(self.grad_full.data_ptr(), self.D, self.gx_stride, self.gx_stride,
+                                                 self.code, prev.data_ptr(), prev.numel(), zs.cuda_stream),
+                       "fsa_zero_rows_strided")
         st = main.cuda_stream
         fwd_args = (self.g.rowptr.data_ptr(), self.g.col.data_ptr(), self.N, self.X.data_ptr(), self.D,
                     self.X.stride(0), self.code, seeds.data_ptr(), self.B, self.root_offset, self.k1, self.k2,
@@ -115,17 +121,17 @@ class Fused2HopStep:
                     self.t2.data_ptr(), out.data_ptr(), out.stride(0), self.ws_f.data_ptr(),
                     self.ws_f.numel(), st)
         bwd_args = (grad_out.data_ptr(), self.B, self.D, grad_out.stride(0), self.code,
-                    self.s1.data_ptr(), cur.data_ptr(), self.k1, self.k2, self.N, self.grad.data_ptr(), 0, None,
-                    None, None, self.ws_b.data_ptr(), self.ws_b.numel())
+                    self.s1.data_ptr(), cur.data_ptr(), self.k1, self.k2, self.N, self.grad_full.data_ptr(),
+                    self.gx_stride, self.gx_stride, 0, self.ws_b.data_ptr(), self.ws_b.numel())
         _select_hop1(self.g)  # baked into the captured graph
         _lib.check(lib.fsa_fused_2hop_fwd_phase(*fwd_args, _lib.FSA_FWD_SAMPLE), "fwd SAMPLE")
         if not self.overlap_zero:
-            _lib.check(lib.fsa_fused_2hop_bwd_phase(*bwd_args, st, _lib.FSA_BWD_PLAN), "bwd PLAN")
+            _lib.check(lib.fsa_fused_2hop_bwd_phase_rows(*bwd_args, st, _lib.FSA_BWD_PLAN), "bwd PLAN")
             _lib.check(lib.fsa_fused_2hop_fwd_phase(*fwd_args, _lib.FSA_FWD_GATHER), "fwd GATHER")
             if head is not None:
                 head(out, grad_out)
-            _lib.check(lib.fsa_fused_2hop_bwd_phase(*bwd_args, st, _lib.FSA_BWD_TERMS), "bwd TERMS")
-            _lib.check(lib.fsa_fused_2hop_bwd_phase(*bwd_args, st, _lib.FSA_BWD_ROWS), "bwd ROWS")
+            _lib.check(lib.fsa_fused_2hop_bwd_phase_rows(*bwd_args, st, _lib.FSA_BWD_TERMS), "bwd TERMS")
+            _lib.check(lib.fsa_fused_2hop_bwd_phase_rows(*bwd_args, st, _lib.FSA_BWD_ROWS), "bwd ROWS")
             if tail is not None:
                 tail()
             return
@@ -133,16 +139,16 @@ class Fused2HopStep:
         ps = self.plan
         if head is None:
             zs.wait_stream(main)  # TERMS after the re-zeroing, on the same side stream
-            _lib.check(lib.fsa_fused_2hop_bwd_phase(*bwd_args, zs.cuda_stream, _lib.FSA_BWD_TERMS), "bwd TERMS")
+            _lib.check(lib.fsa_fused_2hop_bwd_phase_rows(*bwd_args, zs.cuda_stream, _lib.FSA_BWD_TERMS), "bwd TERMS")
         ps.wait_stream(main)
-        _lib.check(lib.fsa_fused_2hop_bwd_phase(*bwd_args, ps.cuda_stream, _lib.FSA_BWD_PLAN), "bwd PLAN")
+        _lib.check(lib.fsa_fused_2hop_bwd_phase_rows(*bwd_args, ps.cuda_stream, _lib.FSA_BWD_PLAN), "bwd PLAN")
         _lib.check(lib.fsa_fused_2hop_fwd_phase(*fwd_args, _lib.FSA_FWD_GATHER), "fwd GATHER")
         if head is not None:
             head(out, grad_out)
-            _lib.check(lib.fsa_fused_2hop_bwd_phase(*bwd_args, st, _lib.FSA_BWD_TERMS), "bwd TERMS")
+            _lib.check(lib.fsa_fused_2hop_bwd_phase_rows(*bwd_args, st, _lib.FSA_BWD_TERMS), "bwd TERMS")
             ps.wait_stream(main)
         ps.wait_stream(zs)  # term table written, previous rows zeroed
-        _lib.check(lib.fsa_fused_2hop_bwd_phase(*bwd_args, ps.cuda_stream, _lib.FSA_BWD_ROWS), "bwd ROWS")
+        _lib.check(lib.fsa_fused_2hop_bwd_phase_rows(*bwd_args, ps.cuda_stream, _lib.FSA_BWD_ROWS), "bwd ROWS")
         if tail is not None:
             tail()
         main.wait_stream(ps)
