@@ -849,7 +849,7 @@ def run_fused(args):
                        "arcs": ra.g.num_edges, "max_degree": ra.g.max_degree(), "clocks": alt["clocks"]}
         # second roofline: the sampler is integer-issue bound at alpha=2.1
         aprof = ra.profile(steps=5)
-        samp = {k: v for k, v in aprof.items() if k.startswith("k_sample")}
+        samp = {k: v for k, v in aprof.items() if k.startswith("k_sample") or k == "k_hop1"}
         samp_ms = sum(v[0] * v[1] for v in samp.values())
         peak_d, peak_info = draw_peak(device)
         ach_d = alt["draws"] / (samp_ms / 1e3) if samp_ms else None
