@@ -1,4 +1,3 @@
-ROUNDS=1 ARGS="--config reddit --no-cpu --no-alt --no-unfused --no-train --no-parity --steps 100" bash tools/ab.sh tools/ab/lib_w2.so tools/ab/lib_w3.so
-ROUNDS=1 ARGS="--config reddit --dtype fp32 --no-cpu --no-alt --no-unfused --no-train --no-parity --steps 100" bash tools/ab.sh tools/ab/lib_w2.so tools/ab/lib_w3.so
-ROUNDS=1 ARGS="--no-cpu --no-alt --no-unfused --no-train --no-parity --steps 200" bash tools/ab.sh tools/ab/lib_w2.so tools/ab/lib_w3.so
-ROUNDS=1 ARGS="--config products25 --no-cpu --no-alt --no-unfused --no-train --no-parity --steps 200" bash tools/ab.sh tools/ab/lib_w2.so tools/ab/lib_w3.so
+ROUNDS=2 ARGS="--no-cpu --no-alt --no-unfused --no-train --no-parity --steps 200" bash tools/ab.sh tools/ab/lib_w4.so tools/ab/lib_cpa.so
+ROUNDS=1 ARGS="--config arxiv --no-cpu --no-alt --no-unfused --no-train --no-parity --steps 200" bash tools/ab.sh tools/ab/lib_w4.so tools/ab/lib_cpa.so
+FSA_LIB=tools/ab/lib_cpa.so python tools/timeline.py --reps 1 2>&1 | grep "hop1\|sample2\|multi"
