@@ -159,6 +159,26 @@ def ncu_traffic(kernel):
         return None, files[-1].name
 
 
+def row_ceiling(kind):
+    """Practical ceiling of this path's access pattern at the products shape (153,600 random
+    400-byte rows, 2.45 M-row table, L2 flushed, kernel-only %globaltimer span) from the committed
+    probe run profiles/r02_row_ceiling.jsonl (tools/tma_gather_probe.cu): best register-load
+    read, or the write of whole 64-byte bursts (the padded gradient rows)."""
+    p = ROOT / "profiles" / "r02_row_ceiling.jsonl"
+    try:
+        rows = [json.loads(ln) for ln in p.read_text().splitlines() if ln.strip()]
+    except OSError:
+        return None
+    if kind == "read":
+        c = [r for r in rows if r["variant"].startswith("ldg")]
+    else:
+        c = [r for r in rows if r["variant"] == "write_rows" and r["p1"] == r["p2"] == 448]
+    if not c:
+        return None
+    best = max(c, key=lambda r: r["gbs"])
+    return {"gbs": best["gbs"], "probe": best, "source": str(p.relative_to(ROOT))}
+
+
 def measured_peak_hbm():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -733,8 +753,14 @@ def run_fused(args):
     # the committed capture is of the products alpha=3 step (tools/profile_step.py defaults)
     traffic, traffic_src = ncu_traffic(dom) if (args.config == "products" and args.alpha == 3.0
                                                 and E == 4) else (None, None)
+    ceil_kind = {"k_gather2": "read", "k_bwd_single": "write"}.get(dom)
+    ceiling = row_ceiling(ceil_kind) if (ceil_kind and args.config in ("products", "products25")
+                                         and E == 4) else None
+    if ceiling and achieved:
+        ceiling["frac"] = achieved / ceiling["gbs"]
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "frac": (achieved / peak) if achieved else None, "random_row_ceiling": ceiling,
+                "traffic": traffic,
                 "traffic_source": traffic_src, "alg_bytes_per_launch": kb,
                 "peak_kind": peak_kind, "kernel_ms": dom_ms,
                 "share_of_step": prof[dom][0] * prof[dom][1] / main["ms_local"],
