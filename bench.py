@@ -66,6 +66,9 @@ def parse_args():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--profile", action="store_true", help="print the per-kernel table to stderr")
     p.add_argument("--eager", action="store_true", help="no CUDA graphs for the device-resident measurement")
+    p.add_argument("--pipeline", action="store_true",
+                   help="time pipelined back-to-back steps (executor pipeline=True: step i+1's forward beside "
+                        "step i's backward) instead of single steps with an L2 flush before each")
     p.add_argument("--flush", default="read", choices=["read", "write", "none"],
                    help="L2 flush between timed steps: read 512 MiB (evicts, leaves L2 clean), write "
                         "512 MiB (evicts, leaves L2 dirty: its write-back lands in the timed step), none")
@@ -274,8 +277,9 @@ class Runner:
         self.flush_sink = torch.zeros(1, dtype=torch.int64, device=device)
         from paper_2511_13645_b200.executor import Fused2HopStep
         self.ex = Fused2HopStep(self.g, self.X, self.B, self.k1, self.k2, root_offset=self.root_offset,
-                                use_graph=not args.eager)
+                                use_graph=not args.eager, pipeline=args.pipeline)
         self.ex.set_grad_out(self.gout)
+        self.ex_lat = None  # non-pipelined executor for the single-step latency (made on demand)
         self.idx = None
 
     def parity(self, n_batches=2):
@@ -356,6 +360,60 @@ class Runner:
         return out
 
     def timed(self, steps, warmup, flush=True):
+        if self.ex.pipeline:
+            return self.timed_pipelined(steps, warmup)
+        return self.timed_steps(steps, warmup, flush)
+
+    def timed_pipelined(self, steps, warmup):
+        """Throughput of K back-to-back pipelined steps (step i+1's forward overlaps step i's
+        backward): one pair of CUDA events around all K steps, the end event after the backward
+        stream has joined.  No L2 flush (the inputs, 1.5 GB, exceed the 126 MB L2); the host
+        enqueues behind a spin kernel, so the events hold device work only."""
+        torch = self.torch
+        warmup = max(warmup, 4)
+        for i in range(warmup):
+            self.step(i)
+        self.ex.sync_copies()
+        torch.cuda.synchronize(self.device)
+        from paper_2511_13645_b200 import _lib
+        l0 = _lib.launch_count()
+        self.eager_step(0)
+        torch.cuda.synchronize(self.device)
+        per_step = _lib.launch_count() - l0
+        if self.world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize(self.device)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t_wall = time.perf_counter()
+        torch.cuda._sleep(40_000_000 * max(1, steps // 50))  # the host enqueues every step meanwhile
+        a.record()
+        for j in range(steps):
+            self.stage(warmup + j)
+            self.launch()
+        self.ex.sync_copies()  # joins the backward stream
+        b.record()
+        torch.cuda.synchronize(self.device)
+        wall = time.perf_counter() - t_wall
+        if self.world > 1:
+            torch.distributed.barrier()
+        ms = a.elapsed_time(b) / steps
+        return [ms] * steps, per_step * steps, wall
+
+    def latency(self, steps, warmup):
+        """Device time of one step alone (non-pipelined executor, L2 flushed before each step)."""
+        if self.ex_lat is None:
+            from paper_2511_13645_b200.executor import Fused2HopStep
+            self.ex_lat = Fused2HopStep(self.g, self.X, self.B, self.k1, self.k2, root_offset=self.root_offset,
+                                        use_graph=not self.args.eager)
+            self.ex_lat.set_grad_out(self.gout)
+        ex, self.ex = self.ex, self.ex_lat
+        try:
+            ms, _, _ = self.timed_steps(steps, warmup, True)
+        finally:
+            self.ex = ex
+        return ms
+
+    def timed_steps(self, steps, warmup, flush=True):
         torch = self.torch
         # at least 4 untimed steps whatever W is: the executor runs each of its two parities
         # eagerly once, then captures each parity's graph, and no capture may fall in the
@@ -693,6 +751,9 @@ def run_fused(args):
         res = {"runner": r, "ms": ms_max, "ms_local": mean_ms, "launches": launches, "clocks": clk.summary(),
                "T1": T1, "T2": T2, "U2": U2, "singles": singles, "draws": r.draws(), "gen_s": r.gen_s,
                "p50": statistics.median(ms), "wall": wall, "parity": parity}
+        if full and r.ex.pipeline:  # one step alone, L2 flushed: the latency the pipeline overlaps
+            lat = max_over_ranks(statistics.mean(r.latency(max(20, args.steps // 2), args.warmup)), world, device)
+            res["latency"] = lat
         if full:
             res["prof"] = r.profile()
             res["e2e"] = r.e2e(max(20, args.steps // 2), 3)
@@ -798,13 +859,20 @@ def run_fused(args):
             "num_nodes": r.N, "arcs": r.g.num_edges, "max_degree": r.g.max_degree(), "alpha": args.alpha,
             "avg_degree_target": shape.avg_degree, "d_feat": D, "batch_per_gpu": B, "global_batch": B * world,
             "fanouts": [k1, k2], "parallelism": f"seed-sharded dp{world} (root_offset), no data-path collective",
-            "l2": {"read": "flushed before every timed step by a 512 MiB read outside the step's CUDA events "
-                           "(evicts L2, leaves it clean); inputs (1.5 GB CSR + features) are larger than L2",
-                   "write": "flushed before every timed step by a 512 MiB write outside the step's CUDA events",
-                   "none": "no flush; inputs (1.5 GB CSR + features, random rows) are larger than L2"}[args.flush],
-            "step_timing": "CUDA events around each step on its stream; the step's inputs are staged into the "
-                           "executor's buffers (copy stream) before its events; the host enqueues 50 steps at a "
-                           "time behind a spin kernel, so the events time device work, not host submission",
+            "l2": ("no flush between pipelined steps: inputs (1.5 GB CSR + features, random rows) are larger "
+                   "than L2; the single-step latency leg flushes L2 before every step"
+                   if r.ex.pipeline else
+                   {"read": "flushed before every timed step by a 512 MiB read outside the step's CUDA events "
+                            "(evicts L2, leaves it clean); inputs (1.5 GB CSR + features) are larger than L2",
+                    "write": "flushed before every timed step by a 512 MiB write outside the step's CUDA events",
+                    "none": "no flush; inputs (1.5 GB CSR + features, random rows) are larger than L2"}[args.flush]),
+            "step_timing": ("K steps back to back through the pipelined executor (step i+1's forward overlaps "
+                            "step i's backward), one pair of CUDA events around all K on the caller's stream after "
+                            "the backward stream joins; value = K x B / that time; the host enqueues behind a "
+                            "spin kernel" if r.ex.pipeline else
+                            "CUDA events around each step on its stream; the step's inputs are staged into the "
+                            "executor's buffers (copy stream) before its events; the host enqueues 50 steps at a "
+                            "time behind a spin kernel, so the events time device work, not host submission"),
             "grad_buffer": "persistent N x D, sparse re-zero of the previous step's rows (fsa_zero_rows) "
                            "on a side stream overlapped with the forward",
             "execution": "eager" if args.eager else "CUDA graph per step (executor.Fused2HopStep)",
@@ -831,6 +899,10 @@ def run_fused(args):
                                  "path": "fused_2hop_forward + fused_2hop_backward(zero='sparse') per call"}},
         "p50_ms": round(main["p50"], 5),
     }
+    if "latency" in main:
+        line["step_latency"] = {"ms": round(main["latency"], 5),
+                                "timing": "one step alone through the non-pipelined executor, L2 flushed by a 512 "
+                                          "MiB read before each step, per-step CUDA events (device work only)"}
     if main["parity"] is not None:
         line["parity"] = main["parity"]
     if strong is not None:

@@ -40,7 +40,8 @@ class Fused2HopStep:
     seeds at global positions ``root_offset + [0, batch)``."""
 
     def __init__(self, graph: CsrGraph, X: torch.Tensor, batch: int, k1: int, k2: int, *,
-                 root_offset: int = 0, use_graph: bool = True, overlap_zero: bool = True):
+                 root_offset: int = 0, use_graph: bool = True, overlap_zero: bool = True,
+                 pipeline: bool = False):
         if X.ndim != 2 or X.shape[0] != graph.num_nodes or X.stride(1) != 1:
             raise ValueError(f"features must be ({graph.num_nodes}, D) row-major")
         if X.dtype not in _DTYPE_CODE:
@@ -54,7 +55,7 @@ class Fused2HopStep:
         self.device = X.device
         self.dtype = X.dtype
         self.code = _DTYPE_CODE[X.dtype]
-        self.use_graph, self.overlap_zero = use_graph, overlap_zero
+        self.use_graph, self.overlap_zero, self.pipeline = use_graph, overlap_zero, pipeline
         dev = self.device
         lib = _lib.load()
         _set_device(dev)
@@ -74,6 +75,8 @@ class Fused2HopStep:
         self.out_copied = [torch.cuda.Event() for _ in range(2)]
         self.out_copied_used = [False, False]
         self.s1 = torch.empty((B, k1), dtype=torch.int32, device=dev)
+        # pipelined: step i+1's forward runs while step i's backward still reads its s1
+        self.s1_p = [self.s1, torch.empty_like(self.s1) if pipeline else self.s1]
         self.s2 = [torch.full((B, k1, k2), -1, dtype=torch.int32, device=dev) for _ in range(2)]
         self.t1 = torch.empty(B, dtype=torch.int32, device=dev)
         self.t2 = torch.empty((B, k1), dtype=torch.int32, device=dev)
@@ -91,6 +94,11 @@ class Fused2HopStep:
         self.parity = 0
         self.graphs = [None, None]
         self.steps_run = 0
+        # pipelined steps: the forward (SAMPLE + GATHER) of step i on the caller's stream, its
+        # backward on self.bwd once that forward is done, so step i+1's forward overlaps it
+        self.bwd = torch.cuda.Stream(device=dev)
+        self.fwd_done = [torch.cuda.Event() for _ in range(2)]
+        self.graphs_b = [None, None]
 
     # -- raw launch sequence of one step (eager or under capture) ----------------------------
     def _launch(self, parity: int, head=None, tail=None) -> None:
@@ -117,11 +125,11 @@ class Fused2HopStep:
         st = main.cuda_stream
         fwd_args = (self.g.rowptr.data_ptr(), self.g.col.data_ptr(), self.N, self.X.data_ptr(), self.D,
                     self.X.stride(0), self.code, seeds.data_ptr(), self.B, self.root_offset, self.k1, self.k2,
-                    0, base_seed.data_ptr(), 1, self.s1.data_ptr(), cur.data_ptr(), self.t1.data_ptr(),
+                    0, base_seed.data_ptr(), 1, self.s1_p[parity].data_ptr(), cur.data_ptr(), self.t1.data_ptr(),
                     self.t2.data_ptr(), out.data_ptr(), out.stride(0), self.ws_f.data_ptr(),
                     self.ws_f.numel(), st)
         bwd_args = (grad_out.data_ptr(), self.B, self.D, grad_out.stride(0), self.code,
-                    self.s1.data_ptr(), cur.data_ptr(), self.k1, self.k2, self.N, self.grad_full.data_ptr(),
+                    self.s1_p[parity].data_ptr(), cur.data_ptr(), self.k1, self.k2, self.N, self.grad_full.data_ptr(),
                     self.gx_stride, self.gx_stride, 0, self.ws_b.data_ptr(), self.ws_b.numel())
         _select_hop1(self.g)  # baked into the captured graph
         _lib.check(lib.fsa_fused_2hop_fwd_phase(*fwd_args, _lib.FSA_FWD_SAMPLE), "fwd SAMPLE")
@@ -152,6 +160,74 @@ class Fused2HopStep:
         if tail is not None:
             tail()
         main.wait_stream(ps)
+
+    # -- pipelined steps: forward and backward as separate launch sequences ---------------------
+    def _args(self, parity: int, st: int):
+        cur = self.s2[parity]
+        seeds, base_seed = self.seeds_p[parity], self.base_seed_p[parity]
+        grad_out, out = self.grad_out_p[parity], self.out_p[parity]
+        fwd_args = (self.g.rowptr.data_ptr(), self.g.col.data_ptr(), self.N, self.X.data_ptr(), self.D,
+                    self.X.stride(0), self.code, seeds.data_ptr(), self.B, self.root_offset, self.k1, self.k2,
+                    0, base_seed.data_ptr(), 1, self.s1_p[parity].data_ptr(), cur.data_ptr(), self.t1.data_ptr(),
+                    self.t2.data_ptr(), out.data_ptr(), out.stride(0), self.ws_f.data_ptr(),
+                    self.ws_f.numel(), st)
+        bwd_args = (grad_out.data_ptr(), self.B, self.D, grad_out.stride(0), self.code,
+                    self.s1_p[parity].data_ptr(), cur.data_ptr(), self.k1, self.k2, self.N, self.grad_full.data_ptr(),
+                    self.gx_stride, self.gx_stride, 0, self.ws_b.data_ptr(), self.ws_b.numel())
+        return fwd_args, bwd_args
+
+    def _launch_fwd(self, parity: int) -> None:
+        """Pipelined step, forward: SAMPLE -> GATHER on the current stream."""
+        lib = _lib.load()
+        fwd_args, _ = self._args(parity, torch.cuda.current_stream(self.device).cuda_stream)
+        _select_hop1(self.g)  # baked into the captured graph
+        _lib.check(lib.fsa_fused_2hop_fwd_phase(*fwd_args, _lib.FSA_FWD_SAMPLE), "fwd SAMPLE")
+        _lib.check(lib.fsa_fused_2hop_fwd_phase(*fwd_args, _lib.FSA_FWD_GATHER), "fwd GATHER")
+
+    def _launch_bwd(self, parity: int) -> None:
+        """Pipelined step, backward (after its forward): the previous step's rows re-zeroed, then
+           zero:  re-zero prev rows ── TERMS ─┐
+           plan:  PLAN ───────────────────────┴── ROWS ── (joined back to the current stream)"""
+        lib = _lib.load()
+        base = torch.cuda.current_stream(self.device)
+        _, bwd_args = self._args(parity, base.cuda_stream)
+        prev = self.s2[1 - parity]
+        zs, ps = self.side, self.plan
+        zs.wait_stream(base)
+        ps.wait_stream(base)
+        with torch.cuda.stream(zs):
+            _lib.check(lib.fsa_zero_rows_strided(self.grad_full.data_ptr(), self.D, self.gx_stride, self.gx_stride,
+                                                 self.code, prev.data_ptr(), prev.numel(), zs.cuda_stream),
+                       "fsa_zero_rows_strided")
+        _lib.check(lib.fsa_fused_2hop_bwd_phase_rows(*bwd_args, zs.cuda_stream, _lib.FSA_BWD_TERMS), "bwd TERMS")
+        _lib.check(lib.fsa_fused_2hop_bwd_phase_rows(*bwd_args, ps.cuda_stream, _lib.FSA_BWD_PLAN), "bwd PLAN")
+        ps.wait_stream(zs)
+        _lib.check(lib.fsa_fused_2hop_bwd_phase_rows(*bwd_args, ps.cuda_stream, _lib.FSA_BWD_ROWS), "bwd ROWS")
+        base.wait_stream(ps)
+
+    def _capture_fn(self, fn, parity: int) -> torch.cuda.CUDAGraph:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn(parity)
+        return g
+
+    def _launch_pipelined(self, p: int, main) -> None:
+        """Step i's forward on ``main``; its backward on self.bwd after that forward.  The caller
+        made ``main`` wait for step i-2's backward (which read this parity's s1 / s2)."""
+        if self.use_graph and self.steps_run >= 2:
+            if self.graphs[p] is None:
+                self.graphs[p] = self._capture_fn(self._launch_fwd, p)
+                self.graphs_b[p] = self._capture_fn(self._launch_bwd, p)
+            self.graphs[p].replay()
+        else:
+            self._launch_fwd(p)
+        self.fwd_done[p].record(main)
+        self.bwd.wait_event(self.fwd_done[p])
+        with torch.cuda.stream(self.bwd):
+            if self.use_graph and self.steps_run >= 2:
+                self.graphs_b[p].replay()
+            else:
+                self._launch_bwd(p)
 
     def _capture(self, parity: int, head=None, tail=None) -> torch.cuda.CUDAGraph:
         # warm the launch path once outside capture (device init, function attributes)
@@ -222,6 +298,21 @@ class Fused2HopStep:
         if self.out_copied_used[p]:  # the previous D2H of out_p[p] must finish before it is rewritten
             main.wait_event(self.out_copied[p])
             self.out_copied_used[p] = False
+        if self.pipeline:
+            if self.done_used[p]:  # step i-2's backward read this parity's s1 / s2
+                main.wait_event(self.done[p])
+            self._launch_pipelined(p, main)
+            self.done[p].record(self.bwd)  # the whole step: its backward follows its forward
+            self.done_used[p] = True
+            if out_host is not None:
+                self.copy_out.wait_event(self.fwd_done[p])
+                with torch.cuda.stream(self.copy_out):
+                    out_host.copy_(self.out_p[p], non_blocking=True)
+                self.out_copied[p].record(self.copy_out)
+                self.out_copied_used[p] = True
+            self.steps_run += 1
+            self.parity = 1 - p
+            return self.out_p[p], SampledIndices2(self.s1_p[p], self.s2[p])
         if self.use_graph:
             if self.steps_run < 2:  # first use of each parity runs eagerly (init, attributes)
                 self._launch(p)
@@ -241,13 +332,16 @@ class Fused2HopStep:
             self.out_copied_used[p] = True
         self.steps_run += 1
         self.parity = 1 - p
-        return self.out_p[p], SampledIndices2(self.s1, self.s2[p])
+        return self.out_p[p], SampledIndices2(self.s1_p[p], self.s2[p])
 
     def sync_copies(self) -> None:
-        """Make the current stream wait for the copy streams (pending D2H of outputs)."""
+        """Make the current stream wait for the copy streams (pending D2H of outputs) and, when
+        pipelined, for the backward stream (the feature gradient of the last step)."""
         cur = torch.cuda.current_stream(self.device)
         cur.wait_stream(self.copy)
         cur.wait_stream(self.copy_out)
+        if self.pipeline:
+            cur.wait_stream(self.bwd)
 
     def kernel_times(self, seeds_list, base_seeds, flush=None) -> dict:
         """Per-kernel device time inside the captured step graph: {name: (ms per launch, launches
