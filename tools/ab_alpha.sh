@@ -1,3 +1,6 @@
-ROUNDS=2 ARGS="--no-cpu --no-alt --no-unfused --no-train --no-parity --steps 200" bash tools/ab.sh tools/ab/lib_w4.so tools/ab/lib_cpa.so
-ROUNDS=1 ARGS="--config arxiv --no-cpu --no-alt --no-unfused --no-train --no-parity --steps 200" bash tools/ab.sh tools/ab/lib_w4.so tools/ab/lib_cpa.so
-FSA_LIB=tools/ab/lib_cpa.so python tools/timeline.py --reps 1 2>&1 | grep "hop1\|sample2\|multi"
+for i in 1 2; do
+python bench.py --no-cpu --no-alt --no-unfused --no-train --no-parity --steps 200 2>/dev/null | python -c "import json,sys;d=json.loads(sys.stdin.read().strip().splitlines()[-1]);print('products', d['ms_per_step'], d['e2e']['value'])"
+python bench.py --config reddit --no-cpu --no-alt --no-unfused --no-train --no-parity --steps 100 2>/dev/null | python -c "import json,sys;d=json.loads(sys.stdin.read().strip().splitlines()[-1]);print('reddit', d['ms_per_step'], d['e2e']['value'])"
+python bench.py --config arxiv --no-cpu --no-alt --no-unfused --no-train --no-parity --steps 200 2>/dev/null | python -c "import json,sys;d=json.loads(sys.stdin.read().strip().splitlines()[-1]);print('arxiv', d['ms_per_step'], d['e2e']['value'])"
+done
+python tools/timeline.py --reps 1 2>&1 | cut -c1-100
