@@ -19,7 +19,7 @@ import torch  # noqa: E402
 
 DBG = ROOT / "tools" / "libfsa_b200_sdbg.so"
 PHASES = ["layout", "setup", "jump", "draws", "next"]
-HOP1_PHASES = ["root", "run", "finish", "jump", "draws"]  # k_hop1 (2-hop forward)
+HOP1_PHASES = ["root", "run", "finish", "prologue", "lane run"]  # k_hop1 (2-hop forward)
 
 
 def main():
