@@ -85,6 +85,39 @@ def test_tune_knobs_validate_arguments(lib):
     assert lib.fsa_tune(99, 1) == _lib.FSA_ERR_ARG
     assert lib.fsa_tune(1, 0) == _lib.FSA_ERR_ARG
     assert lib.fsa_tune(2, 7) == _lib.FSA_ERR_ARG
-    for knob, bad, default in ((3, 9, 1), (4, 65, 8), (5, 0, 4)):
+    for knob, bad, default in ((3, 9, 1), (4, 65, 8), (5, 0, 4), (6, 3, 1), (6, 0, 1)):
         assert lib.fsa_tune(knob, bad) == _lib.FSA_ERR_ARG
         assert lib.fsa_tune(knob, default) == _lib.FSA_OK
+
+
+def test_first_hop_path_choice_by_mean_degree(monkeypatch):
+    """The Python layer picks the 2-hop forward's first-hop path per graph: warp per root below
+    HOP1_TILE_MEAN_DEGREE arcs per node, the tile sampler above; FSA_HOP1 pins it."""
+    import torch
+    from paper_2511_13645_b200 import fused
+    from paper_2511_13645_b200.graph import CsrGraph
+
+    calls = []
+
+    class Lib:
+        def fsa_tune(self, what, value):
+            calls.append((what, value))
+            return 0
+
+    monkeypatch.setattr(fused._lib, "load", lambda *a, **k: Lib())
+    monkeypatch.delenv("FSA_HOP1", raising=False)
+    fused._hop1_set[0] = None
+
+    def graph(n, e):
+        rp = torch.zeros(n + 1, dtype=torch.int32)
+        rp[1:] = e // n
+        return CsrGraph(n, rp, torch.zeros(e, dtype=torch.int32))
+
+    fused._select_hop1(graph(100, 5_000))      # mean 50: warp per root
+    fused._select_hop1(graph(100, 5_000))      # unchanged: no second call
+    fused._select_hop1(graph(100, 50_000))     # mean 500: tiles
+    assert calls == [(6, 1), (6, 2)]
+    monkeypatch.setenv("FSA_HOP1", "1")
+    fused._select_hop1(graph(100, 5_000))      # pinned: left alone
+    assert calls == [(6, 1), (6, 2)]
+    fused._hop1_set[0] = None

@@ -479,3 +479,20 @@ def test_wide_rows_dense_collisions(fsa, oracle_mod, D, dtype):
     k = int(nt)
     assert k == int((hits > 0).sum())
     assert torch.equal(rows[:k], grad[touched[:k].long()])
+
+
+def test_draw_loop_benchmark_hook(fsa):
+    """fsa_bench_draws (the sampler's integer roofline, tools/bench_draws.py): one warp reports
+    clock cycles, a grid of CTAs runs and can be timed; bad geometries are argument errors."""
+    from paper_2511_13645_b200 import _lib
+    lib = _lib.load()
+    out = torch.zeros(2, dtype=torch.int64, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    for mode in range(4):
+        _lib.check(lib.fsa_bench_draws(mode, 1024, 20000, 10, 32, out.data_ptr(), st), "one warp")
+        torch.cuda.synchronize()
+        assert 0 < int(out[0]) < 1024 * 10_000  # cycles for 1,024 draws per lane
+        _lib.check(lib.fsa_bench_draws(mode, 512, 20000, 10, 148 * 256, out.data_ptr(), st), "grid")
+        torch.cuda.synchronize()
+    assert lib.fsa_bench_draws(0, 1000, 20000, 10, 32, out.data_ptr(), st) == _lib.FSA_ERR_ARG  # n % 256
+    assert lib.fsa_bench_draws(0, 512, 20000, 10, 300, out.data_ptr(), st) == _lib.FSA_ERR_ARG  # lanes % 256
