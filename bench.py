@@ -927,7 +927,7 @@ def run_fused(args):
                       "speedup_of_fused": round(pc[impl][0] / fused_ms, 3),
                       "materialised_bytes_per_step": pc[impl][1]} for impl in ("unfused", "unfused_dedup")},
             "unit": "seeds/s"}
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu:  # the CPU baseline is an N=1 figure
         times, threads = cpu_oracle_time(r, args.cpu_seconds, max_steps=30)
         cpu_ms = statistics.median(times) * 1e3
         line["cpu_baseline"] = {"value": round(B / (cpu_ms / 1e3), 2), "unit": "seeds/s", "cores": threads,
@@ -959,7 +959,7 @@ def run_fused(args):
             "peak_kind": "measured: k_sample's draw loop on every resident warp (fsa_bench_draws)",
             "peak_detail": peak_info,
             "kernels_ms": {k: round(v[0], 5) for k, v in sorted(aprof.items())}}
-        if rank == 0 and not args.no_cpu:
+        if rank == 0 and world == 1 and not args.no_cpu:  # the CPU baseline is an N=1 figure
             times, threads = cpu_oracle_time(ra, args.cpu_seconds, max_steps=10)
             line["alt"]["cpu_baseline"] = {"value": round(B / statistics.median(times), 2), "unit": "seeds/s",
                                            "cores": threads, "kind": "port",
