@@ -14,7 +14,7 @@ Sampler paths and the cases that reach them (paper_2511_13645_b200/csrc/fsa_kern
   * short buckets, Barrett remainder (m < FAST_M = 16,384): every shape;
   * fraction fast path (m >= FAST_M): hub rows of the alpha=2.1 shapes, ``test_fraction_path_hubs``;
   * long buckets (SEG > 256 draws: the chunk loop with modulus re-staging): ``test_long_buckets``
-    (bucket divisor forced so that SEG reaches 4,096) and the alpha=2.1 products shape;
+    (bucket divisor forced so that SEG reaches its maximum, 512) and the alpha=2.1 products shape;
   * moduli beyond the table (m >= 2^21, constants computed inline): ``test_star_beyond_table``;
   * 64-bit remainder (m > 2^30): ``test_row_longer_than_2_pow_30``.
 """
@@ -218,7 +218,7 @@ def test_fraction_path_hubs(fsa, oracle):
 
 
 def test_long_buckets(fsa, oracle):
-    """Bucket divisor forced high (fsa_tune 1): the sampler picks SEG up to 4,096 draws per lane,
+    """Bucket divisor forced high (fsa_tune 1): the sampler picks SEG up to 512 draws per lane,
     so the long-bucket chunk loop (modulus constants re-staged every 256 draws) runs at both
     hops, on the hub graph (fraction path) and on the alpha=2.1 arxiv shape (Barrett path)."""
     from paper_2511_13645_b200 import _lib
