@@ -265,7 +265,8 @@ int fsa_baseline_2hop_bwd(const void* grad_out, int64_t B, int64_t D, int64_t g_
  * divisor (value >= 1, default 2); what = 2, the gather's L2 prefetch of a root's rows (0/1,
  * default 0); what = 3, CTAs per SM of the sparse re-zero (1..8, default 1); what = 4, CTAs per SM of the
  * backward's slot count (1..64, default 8); what = 5, CTAs per SM of the multi-hit row
- * writer (1..8, default 4); what = 6, the 2-hop forward's first hop (1: one warp per root
+ * writer (1..8; 0, the default: 2, launched beside the singles, for rows wider than one
+ * 32-lane chunk span, else 4 after them); what = 6, the 2-hop forward's first hop (1: one warp per root
  * samples, finalises and plans it in one kernel, the default; 2: the tile sampler with
  * separate planning passes, faster for dense graphs with long first-hop chains). */
 int fsa_tune(int what, int value);

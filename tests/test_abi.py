@@ -80,12 +80,13 @@ def test_product_package_does_not_import_the_oracle():
 
 def test_tune_knobs_validate_arguments(lib):
     """fsa_tune: unknown knobs and out-of-range values are argument errors; the host-side knobs
-    (3: re-zero CTAs, 4: count CTAs, 5: multi-hit CTAs) set without a device and restore."""
+    (3: re-zero CTAs, 4: count CTAs, 5: multi-hit CTAs, 6: first-hop path) set without a device
+    and restore."""
     from paper_2511_13645_b200 import _lib
     assert lib.fsa_tune(99, 1) == _lib.FSA_ERR_ARG
     assert lib.fsa_tune(1, 0) == _lib.FSA_ERR_ARG
     assert lib.fsa_tune(2, 7) == _lib.FSA_ERR_ARG
-    for knob, bad, default in ((3, 9, 1), (4, 65, 8), (5, 0, 4), (6, 3, 1), (6, 0, 1)):
+    for knob, bad, default in ((3, 9, 1), (4, 65, 8), (5, 9, 0), (5, -1, 0), (6, 3, 1), (6, 0, 1)):
         assert lib.fsa_tune(knob, bad) == _lib.FSA_ERR_ARG
         assert lib.fsa_tune(knob, default) == _lib.FSA_OK
 
