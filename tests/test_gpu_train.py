@@ -1,4 +1,5 @@
-"""GPU SAGE training step (train.py) against a numpy restatement of the reference step
+"""GPU SAGE training step (train.py) against the reference's own train_step (golden vectors,
+tests/golden/train_steps.npz) and a numpy restatement of the reference step
 (pkg/src/fsa/train.py:111-251) fed the oracle's aggregation: loss, parameters and moments must
 agree to fp32 GEMM tolerance step after step; the fused feature gradient bitwise."""
 
@@ -141,3 +142,38 @@ def test_graph_train_step_matches_eager(golden_powerlaw, use_graph):
             torch.testing.assert_close(getattr(s_graph, k), getattr(s_eager, k), rtol=1e-6, atol=1e-7)
         torch.testing.assert_close(gts.feature_grad, gbuf, rtol=1e-6, atol=1e-7)
     assert s_graph.step_count == s_eager.step_count == 6
+
+
+@pytest.mark.parametrize("variant", ["fused", "baseline"])
+def test_train_step_matches_reference_goldens(variant):
+    """Four train_step calls from init_train_state(D, 32, 5, base_seed=42) against the reference's
+    own train_step run on the same batches (tests/golden/train_steps.npz, made by
+    tests/golden/make_train_golden.py from pkg/src/fsa/train.py:185-251): losses, sampled pairs,
+    parameters, AdamW moments and the feature-gradient buffer after every step."""
+    from conftest import load_golden
+    import paper_2511_13645_b200 as fsa
+    from paper_2511_13645_b200 import train
+
+    gt = load_golden("train_steps.npz")
+    pl = load_golden("powerlaw_cases.npz")
+    N, D, k1, k2, H, C, seed = (int(x) for x in gt["meta"])
+    g = fsa.CsrGraph.from_arrays(pl["pl30_rowptr"], pl["pl30_col"], device="cuda", num_nodes=N)
+    Xd = torch.as_tensor(pl["pl30_X"].astype(np.float32)).cuda()
+    state = train.init_train_state(D, H, C, base_seed=seed)
+    gbuf = torch.zeros((N, D), device="cuda")
+    p = variant[0]
+    for s in range(len(gt["seeds"])):
+        batch = fsa.SeedBatch(gt["seeds"][s], gt["labels"][s])
+        res = train.train_step(g, Xd, batch, (k1, k2), fsa.step_seed(seed, s), variant, state, grad_scratch=gbuf)
+        assert res.sampled_pairs == int(gt[f"{p}{s}_pairs"]), s
+        assert bool(res.grads_applied) == bool(gt[f"{p}{s}_applied"])
+        assert abs(float(res.loss) - float(gt[f"{p}{s}_loss"])) < 1e-5, s
+        for k in train.PARAM_NAMES:
+            np.testing.assert_allclose(getattr(state, k).cpu().numpy(), gt[f"{p}{s}_{k}"], rtol=1e-3, atol=1e-5)
+            np.testing.assert_allclose(state.m[k].cpu().numpy(), gt[f"{p}{s}_m_{k}"], rtol=1e-3, atol=1e-7)
+            np.testing.assert_allclose(state.v[k].cpu().numpy(), gt[f"{p}{s}_v_{k}"], rtol=1e-3, atol=1e-9)
+        gb = gbuf.cpu().numpy()
+        rows = np.flatnonzero(np.any(gb != 0, axis=1))
+        np.testing.assert_array_equal(rows, gt[f"{p}{s}_grow"])
+        np.testing.assert_allclose(gb[rows], gt[f"{p}{s}_gval"], rtol=1e-3, atol=1e-6)
+    assert state.step_count == len(gt["seeds"])
