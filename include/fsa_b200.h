@@ -262,7 +262,7 @@ int fsa_baseline_2hop_bwd(const void* grad_out, int64_t B, int64_t D, int64_t g_
                           void* stream);
 
 /* Performance knobs for experiments (results never change): what = 1, the sampler's bucket-length
- * divisor (value >= 1, default 2); what = 2, the gather's L2 prefetch of a root's rows (0/1,
+ * divisor (value >= 1; 0, the default: 1 for a phase of >= 2^24 draws, else 2); what = 2, the gather's L2 prefetch of a root's rows (0/1,
  * default 0); what = 3, CTAs per SM of the sparse re-zero (1..8, default 1); what = 4, CTAs per SM of the
  * backward's slot count (1..64, default 8); what = 5, CTAs per SM of the multi-hit row
  * writer (1..8; 0, the default: 2, launched beside the singles, for rows wider than one

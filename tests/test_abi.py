@@ -84,7 +84,7 @@ def test_tune_knobs_validate_arguments(lib):
     and restore."""
     from paper_2511_13645_b200 import _lib
     assert lib.fsa_tune(99, 1) == _lib.FSA_ERR_ARG
-    assert lib.fsa_tune(1, 0) == _lib.FSA_ERR_ARG
+    assert lib.fsa_tune(1, -1) == _lib.FSA_ERR_ARG
     assert lib.fsa_tune(2, 7) == _lib.FSA_ERR_ARG
     for knob, bad, default in ((3, 9, 1), (4, 65, 8), (5, 9, 0), (5, -1, 0), (6, 3, 1), (6, 0, 1)):
         assert lib.fsa_tune(knob, bad) == _lib.FSA_ERR_ARG

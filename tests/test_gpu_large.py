@@ -231,7 +231,7 @@ def test_long_buckets(fsa, oracle):
         hub.run_api(oracle, B=512, n=1)
         shape_case(fsa, "arxiv", 2.1).run_api(oracle, n=1)
     finally:
-        _lib.check(lib.fsa_tune(1, 2), "fsa_tune")  # back to the default
+        _lib.check(lib.fsa_tune(1, 0), "fsa_tune")  # back to the default (auto)
 
 
 @pytest.fixture
