@@ -273,6 +273,23 @@ int fsa_tune(int what, int value);
 /* out[i] = x[i] % m[i] through the Barrett path used by the sampler (2 <= m <= 2^30) */
 int fsa_umod(const uint64_t* x, const uint32_t* m, int64_t n, uint32_t* out, void* stream);
 
+/* Row stage of the training step's SAGE-mean classifier head (fp32; with two library GEMMs it
+ * replaces head_forward + cross_entropy + head_backward, pkg/src/fsa/train.py:111-160). For B
+ * seeds: concat = [X[seeds] | agg], hidden = ReLU(concat W1 + b1), logits = hidden W2 + b2, the
+ * softmax cross-entropy against labels, dlogits = (softmax - onehot) / B, dhidden, and
+ * d agg -> grad_agg [B x D] (row stride grad_stride). The workspace receives, in order (each
+ * region 256-byte aligned): [concat | 1] [B x (2D+1)], [hidden | 1] [B x (H+1)], dhidden [B x H],
+ * dlogits [B x C] and the per-row losses [B], so that [concat | 1]^T dhidden = [dW1; db1],
+ * [hidden | 1]^T dlogits = [dW2; db2] and loss = mean(row losses). Row-major, element strides;
+ * H % 4 == 0, H <= 512, W1 / W2 16-byte aligned. Labels outside [0, C) give NaN rows. One
+ * kernel on `stream`. */
+size_t fsa_sage_head_ws_bytes(int64_t B, int32_t D, int32_t H, int32_t C);
+size_t fsa_sage_head_smem_bytes(int32_t D, int32_t H, int32_t C);
+int fsa_sage_head_rows(const float* X, int64_t x_stride, const int64_t* seeds, const float* agg, int64_t agg_stride,
+                       const int64_t* labels, int64_t B, int32_t D, int32_t H, int32_t C, const float* W1,
+                       const float* b1, const float* W2, const float* b2, float* grad_agg, int64_t grad_stride,
+                       void* ws, size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -16,7 +16,7 @@ from pathlib import Path
 PKG_DIR = Path(__file__).resolve().parent
 CSRC = PKG_DIR / "csrc"
 LIB_PATH = PKG_DIR / "libfsa_b200.so"
-SOURCES = [CSRC / "fsa_kernels.cu"]
+SOURCES = [CSRC / "fsa_kernels.cu", CSRC / "fsa_head.cu"]
 DEPS = SOURCES + [CSRC / "fsa_rng.cuh", PKG_DIR.parent / "include" / "fsa_b200.h"]
 
 NVCC_FLAGS = [

@@ -1,0 +1,279 @@
+// SAGE-mean classifier head of the training step (reference: pkg/src/fsa/train.py:111-160), fp32.
+//
+//   k_head_rows    one CTA per R seed rows: concat = [X[seed] | x_agg] staged in shared memory,
+//                  hidden = ReLU(concat W1 + b1), logits = hidden W2 + b2, the max-shifted softmax
+//                  cross-entropy per row, dlogits = (softmax - onehot) / B, dhidden =
+//                  (dlogits W2^T) * (hidden > 0), and d_x_agg = dhidden W1[D:]^T (the rows the
+//                  replay backward scatters). W2 sits in shared memory; W1 streams through a ring
+//                  of cp.async-filled chunk buffers with HEAD_S - 1 chunks in flight (once for the
+//                  forward, once for d_x_agg), so the L2 round trips overlap.
+//   The kernel also writes [concat | 1] and [hidden | 1] and dlogits for the caller's two
+//   parameter GEMMs ([concat | 1]^T dhidden = [dW1; db1], [hidden | 1]^T dlogits = [dW2; db2]) and
+//   the per-row losses.
+//
+// Labels outside [0, C) make the row's loss and gradients NaN, so the step's finiteness check
+// discards the update (the reference raises an IndexError there).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "../../include/fsa_b200.h"
+
+namespace {
+
+constexpr int HEAD_THREADS = 256;
+constexpr int HEAD_R = 8;    // seed rows per CTA
+constexpr int HEAD_KC = 16;  // W1 rows per staged chunk
+constexpr int HEAD_S = 4;    // chunk buffers in the cp.async ring (HEAD_S - 1 chunks in flight)
+
+__device__ __forceinline__ float warp_sum(float v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ void cpa16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+struct HeadArgs {
+  const float* X; int64_t xs; const int64_t* seeds; const float* agg; int64_t as; const int64_t* labels;
+  int B, D, H, C;
+  const float* W1; const float* b1; const float* W2; const float* b2;
+  float* gagg; int64_t gs;
+  float* cat1; float* hid1; float* dhid; float* dlog; float* lrow;  // outputs for the parameter GEMMs
+};
+
+// chunk c of rows [base, base + total) of W1 (row length H, H % 4 == 0) into ring slot c % HEAD_S via
+// 16-byte cp.async, one commit group per chunk (an empty group past the end keeps the count uniform)
+__device__ __forceinline__ void stage_w1(float* ring, const float* W1, int H, int base, int total, int c) {
+  const int k0 = c * HEAD_KC, n = min(HEAD_KC, total - k0);
+  if (n > 0) {
+    float* buf = ring + (c % HEAD_S) * HEAD_KC * H;
+    const int q = H >> 2, cnt = n * q;
+    const float* src = W1 + (int64_t)(base + k0) * H;
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) cpa16(buf + i * 4, src + i * 4);
+  }
+  cpa_commit();
+}
+
+template <int R>
+__global__ void __launch_bounds__(HEAD_THREADS) k_head_rows(HeadArgs a) {
+  extern __shared__ __align__(16) float sm[];
+  const int D = a.D, D2 = 2 * D, H = a.H, C = a.C;
+  float* ring = sm;                        // [HEAD_S][KC][H] W1 chunk ring
+  float* w2 = ring + HEAD_S * HEAD_KC * H;  // [H][C]
+  float* hh = w2 + ((H * C + 3) & ~3);  // [R][H]
+  float* dh = hh + R * H;            // [R][H]
+  float* dl = dh + R * H;            // [R][C]
+  float* cc = dl + R * C;            // [R][2D]
+  const int r0 = blockIdx.x * R;
+  const int nr = min(R, a.B - r0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+
+  {  // W2 (whole) and the first W1 chunk in flight while the concat rows load
+    const int q = (H * C) >> 2;
+    for (int i = threadIdx.x; i < q; i += blockDim.x) cpa16(w2 + i * 4, a.W2 + i * 4);
+    cpa_commit();
+  }
+  const int nch = (D2 + HEAD_KC - 1) / HEAD_KC;
+  for (int c = 0; c < HEAD_S - 1; ++c) stage_w1(ring, a.W1, H, 0, D2, c);
+  for (int i = threadIdx.x; i < R * D2; i += blockDim.x) {
+    const int r = i / D2, k = i - r * D2;
+    float v = 0.f;
+    if (r < nr) {
+      const int64_t row = r0 + r;
+      v = k < D ? a.X[a.seeds[row] * a.xs + k] : a.agg[row * a.as + (k - D)];
+    }
+    cc[i] = v;
+  }
+
+  // hidden = ReLU(concat W1 + b1): thread j keeps R accumulators per column it owns
+  constexpr int JMAX = 2;  // H <= JMAX * blockDim.x
+  float acc[JMAX][R];
+#pragma unroll
+  for (int u = 0; u < JMAX; ++u)
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[u][r] = 0.f;
+  for (int c = 0; c < nch; ++c) {
+    const int k0 = c * HEAD_KC, n = min(HEAD_KC, D2 - k0);
+    stage_w1(ring, a.W1, H, 0, D2, c + HEAD_S - 1);  // into the slot read in iteration c - 1
+    cpa_wait<HEAD_S - 1>();
+    __syncthreads();
+    const float* w = ring + (c % HEAD_S) * HEAD_KC * H;
+#pragma unroll
+    for (int u = 0; u < JMAX; ++u) {
+      const int j = threadIdx.x + u * blockDim.x;
+      if (j < H) {
+        for (int t = 0; t < n; ++t) {
+          const float wv = w[t * H + j];
+#pragma unroll
+          for (int r = 0; r < R; ++r) acc[u][r] = fmaf(cc[r * D2 + k0 + t], wv, acc[u][r]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // the d_x_agg pass streams W1[D:] through the same buffers: start its first chunk now
+  const int nch2 = (D + HEAD_KC - 1) / HEAD_KC;
+  for (int c = 0; c < HEAD_S - 1; ++c) stage_w1(ring, a.W1, H, D, D, c);
+#pragma unroll
+  for (int u = 0; u < JMAX; ++u) {
+    const int j = threadIdx.x + u * blockDim.x;
+    if (j < H) {
+      const float bj = a.b1[j];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const float h = acc[u][r] + bj;
+        hh[r * H + j] = h > 0.f ? h : 0.f;
+      }
+    }
+  }
+  __syncthreads();
+
+  for (int i = threadIdx.x; i < R * C; i += blockDim.x) {  // logits = hidden W2 + b2
+    const int r = i / C, c = i - r * C;
+    float s = 0.f;
+    const float* hr = hh + r * H;
+    for (int j = 0; j < H; ++j) s = fmaf(hr[j], w2[j * C + c], s);
+    dl[i] = s + a.b2[c];
+  }
+  __syncthreads();
+
+  for (int r = warp; r < R; r += nw) {  // softmax cross-entropy, dlogits (train.py:123-139)
+    float* L = dl + r * C;
+    if (r >= nr) {  // padding rows: keep them finite and inert
+      for (int c = lane; c < C; c += 32) L[c] = 0.f;
+      continue;
+    }
+    float m = -INFINITY;
+    for (int c = lane; c < C; c += 32) m = fmaxf(m, L[c]);
+    m = warp_max(m);
+    float s = 0.f;
+    for (int c = lane; c < C; c += 32) s += expf(L[c] - m);
+    s = warp_sum(s);
+    const float lse = logf(s);
+    const int64_t y = a.labels[r0 + r];
+    const bool bad = y < 0 || y >= C;
+    const float ly = bad ? NAN : (L[bad ? 0 : y] - m) - lse;
+    __syncwarp();
+    const float fB = (float)a.B;
+    for (int c = lane; c < C; c += 32) {
+      const float p = expf(L[c] - m) / s;
+      L[c] = bad ? NAN : (p - (c == y ? 1.f : 0.f)) / fB;
+    }
+    if (lane == 0) a.lrow[r0 + r] = -ly;
+  }
+  __syncthreads();
+
+  for (int j = threadIdx.x; j < H; j += blockDim.x) {  // dhidden = (dlogits W2^T) * (hidden > 0)
+    float s[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) s[r] = 0.f;
+    for (int c = 0; c < C; ++c) {
+      const float w = w2[j * C + c];
+#pragma unroll
+      for (int r = 0; r < R; ++r) s[r] = fmaf(dl[r * C + c], w, s[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) dh[r * H + j] = s[r] * (hh[r * H + j] > 0.f ? 1.f : 0.f);
+  }
+  // (the chunk loop's first barrier orders these dh writes before their reads)
+
+  for (int c = 0; c < nch2; ++c) {  // d_x_agg[r][k] = sum_j dhidden[r][j] W1[D + k][j]
+    const int k0 = c * HEAD_KC, n = min(HEAD_KC, D - k0);
+    stage_w1(ring, a.W1, H, D, D, c + HEAD_S - 1);
+    cpa_wait<HEAD_S - 1>();
+    __syncthreads();
+    const float* w = ring + (c % HEAD_S) * HEAD_KC * H;
+    for (int t = warp; t < n; t += nw) {
+      float s[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) s[r] = 0.f;
+      for (int j = lane; j < H; j += 32) {
+        const float wj = w[t * H + j];
+#pragma unroll
+        for (int r = 0; r < R; ++r) s[r] = fmaf(dh[r * H + j], wj, s[r]);
+      }
+      float mine = 0.f;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const float v = warp_sum(s[r]);
+        if (lane == r) mine = v;
+      }
+      if (lane < nr) a.gagg[(int64_t)(r0 + lane) * a.gs + k0 + t] = mine;
+    }
+    __syncthreads();
+  }
+
+  const int D21 = D2 + 1, H1 = H + 1;  // [concat | 1], [hidden | 1], dhidden, dlogits rows
+  for (int i = threadIdx.x; i < nr * D21; i += blockDim.x) {
+    const int r = i / D21, k = i - r * D21;
+    a.cat1[(int64_t)(r0 + r) * D21 + k] = k < D2 ? cc[r * D2 + k] : 1.f;
+  }
+  for (int i = threadIdx.x; i < nr * H1; i += blockDim.x) {
+    const int r = i / H1, j = i - r * H1;
+    a.hid1[(int64_t)(r0 + r) * H1 + j] = j < H ? hh[r * H + j] : 1.f;
+  }
+  for (int i = threadIdx.x; i < nr * H; i += blockDim.x) a.dhid[(int64_t)r0 * H + i] = dh[i];
+  for (int i = threadIdx.x; i < nr * C; i += blockDim.x) a.dlog[(int64_t)r0 * C + i] = dl[i];
+}
+
+inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+size_t rows_smem(int D, int H, int C) {
+  return ((size_t)HEAD_S * HEAD_KC * H + (((size_t)H * C + 3) & ~(size_t)3) + (size_t)HEAD_R * (2 * H + C + 2 * D)) *
+         sizeof(float);
+}
+
+}  // namespace
+
+extern "C" size_t fsa_sage_head_ws_bytes(int64_t B, int32_t D, int32_t H, int32_t C) {
+  if (B <= 0 || D <= 0 || H <= 0 || C <= 0) return 0;
+  return align_up((size_t)B * (2 * D + 1) * 4) + align_up((size_t)B * (H + 1) * 4) + align_up((size_t)B * H * 4) +
+         align_up((size_t)B * C * 4) + align_up((size_t)B * 4);
+}
+
+extern "C" size_t fsa_sage_head_smem_bytes(int32_t D, int32_t H, int32_t C) {
+  if (D <= 0 || H <= 0 || C <= 0) return 0;
+  return rows_smem(D, H, C);
+}
+
+extern "C" int fsa_sage_head_rows(const float* X, int64_t x_stride, const int64_t* seeds, const float* agg,
+                                  int64_t agg_stride, const int64_t* labels, int64_t B, int32_t D, int32_t H,
+                                  int32_t C, const float* W1, const float* b1, const float* W2, const float* b2,
+                                  float* grad_agg, int64_t grad_stride, void* ws, size_t ws_bytes, void* stream) {
+  if (B <= 0 || B > (1 << 30) || D <= 0 || H <= 0 || C <= 0 || x_stride < D || agg_stride < D ||
+      grad_stride < D || H > 2 * HEAD_THREADS)
+    return FSA_ERR_ARG;
+  if (!X || !seeds || !agg || !labels || !W1 || !b1 || !W2 || !b2 || !grad_agg || !ws) return FSA_ERR_ARG;
+  if ((H & 3) || (reinterpret_cast<uintptr_t>(W1) & 15) || (reinterpret_cast<uintptr_t>(W2) & 15))
+    return FSA_ERR_ALIGN;
+  if (ws_bytes < fsa_sage_head_ws_bytes(B, D, H, C)) return FSA_ERR_WORKSPACE;
+  const size_t smem = rows_smem(D, H, C);
+  if (smem > 227 * 1024) return FSA_ERR_ARG;
+  char* p = static_cast<char*>(ws);
+  HeadArgs a{X, x_stride, seeds, agg, agg_stride, labels, (int)B, D, H, C, W1, b1, W2, b2, grad_agg, grad_stride};
+  a.cat1 = reinterpret_cast<float*>(p);
+  p += align_up((size_t)B * (2 * D + 1) * 4);
+  a.hid1 = reinterpret_cast<float*>(p);
+  p += align_up((size_t)B * (H + 1) * 4);
+  a.dhid = reinterpret_cast<float*>(p);
+  p += align_up((size_t)B * H * 4);
+  a.dlog = reinterpret_cast<float*>(p);
+  p += align_up((size_t)B * C * 4);
+  a.lrow = reinterpret_cast<float*>(p);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaFuncSetAttribute(k_head_rows<HEAD_R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return FSA_ERR_CUDA;
+  k_head_rows<HEAD_R><<<(unsigned)((B + HEAD_R - 1) / HEAD_R), HEAD_THREADS, smem, st>>>(a);
+  e = cudaGetLastError();
+  return e == cudaSuccess ? FSA_OK : FSA_ERR_CUDA;
+}

@@ -177,3 +177,47 @@ def test_train_step_matches_reference_goldens(variant):
         np.testing.assert_array_equal(rows, gt[f"{p}{s}_grow"])
         np.testing.assert_allclose(gb[rows], gt[f"{p}{s}_gval"], rtol=1e-3, atol=1e-6)
     assert state.step_count == len(gt["seeds"])
+
+
+@pytest.mark.parametrize("B,D,H,C", [(1024, 100, 256, 47), (1000, 602, 256, 41), (37, 128, 64, 5)])
+def test_sage_head_kernels_match_torch_fp64(B, D, H, C):
+    """fsa_sage_head_fwd_bwd (the CUDA head of the training step) against the library head
+    (head_forward + cross_entropy + head_backward, train.py:111-160) run in fp64."""
+    from paper_2511_13645_b200 import train
+    gen = torch.Generator(device="cuda").manual_seed(B + D)
+    N = 5000
+    X = torch.randn(N, D + 3, device="cuda", generator=gen)[:, :D]  # strided rows
+    seeds = torch.randint(0, N, (B,), device="cuda", generator=gen)
+    agg = torch.randn(B, D, device="cuda", generator=gen)
+    labels = torch.randint(0, C, (B,), device="cuda", generator=gen)
+    state = train.init_train_state(D, H, C, base_seed=3)
+    state.b1.normal_(generator=gen)  # non-zero biases exercise the bias paths
+    state.b2.normal_(generator=gen)
+    loss, grads, dx = train.sage_head(X, seeds, agg, labels, state)
+    s64 = train.init_train_state(D, H, C, base_seed=3, dtype=torch.float64)
+    for n in train.PARAM_NAMES:
+        getattr(s64, n).copy_(getattr(state, n))
+    logits, cache = train.head_forward(X.double().index_select(0, seeds), agg.double(), s64)
+    l64, dl = train.cross_entropy(logits, labels)
+    g64, _, dx64 = train.head_backward(dl, cache, s64)
+    torch.testing.assert_close(loss.double(), l64, rtol=1e-5, atol=1e-6)
+    torch.testing.assert_close(dx.double(), dx64, rtol=1e-4, atol=1e-7)
+    for n in train.PARAM_NAMES:
+        torch.testing.assert_close(grads[n].double(), g64[n], rtol=1e-4, atol=1e-7)
+
+
+def test_sage_head_bad_label_gives_nonfinite_update_skip():
+    from paper_2511_13645_b200 import train
+    B, D, H, C = 64, 16, 32, 4
+    X = torch.randn(100, D, device="cuda")
+    seeds = torch.arange(B, device="cuda")
+    agg = torch.randn(B, D, device="cuda")
+    labels = torch.zeros(B, dtype=torch.int64, device="cuda")
+    labels[5] = C  # out of range
+    state = train.init_train_state(D, H, C, base_seed=1)
+    before = {k: getattr(state, k).clone() for k in train.PARAM_NAMES}
+    loss, grads, _ = train.sage_head(X, seeds, agg, labels, state)
+    assert not torch.isfinite(loss)
+    assert not bool(train.adamw_step(state, grads))
+    for k in train.PARAM_NAMES:
+        assert torch.equal(getattr(state, k), before[k])

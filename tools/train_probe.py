@@ -52,3 +52,21 @@ with profile(activities=[ProfilerActivity.CUDA]) as prof:
         one(i)
     torch.cuda.synchronize()
 print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=40, max_name_column_width=60))
+
+# the head alone (no concurrent backward PLAN kernels): sage_head on this step's shapes
+out = torch.randn(1024, sh.d_feat, device=dev)
+gagg = torch.empty_like(out)
+for _ in range(3):
+    tr.sage_head(X, batches[0], out, lab[0], state, grad_agg=gagg)
+torch.cuda.synchronize()
+a.record()
+for _ in range(50):
+    tr.sage_head(X, batches[0], out, lab[0], state, grad_agg=gagg)
+b.record()
+torch.cuda.synchronize()
+print(f"sage_head alone: {a.elapsed_time(b) / 50 * 1e3:.1f} us per call (host-bound if close to the enqueue time)")
+with profile(activities=[ProfilerActivity.CUDA]) as prof:
+    for _ in range(10):
+        tr.sage_head(X, batches[0], out, lab[0], state, grad_agg=gagg)
+    torch.cuda.synchronize()
+print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=12, max_name_column_width=60))
