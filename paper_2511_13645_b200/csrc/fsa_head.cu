@@ -22,9 +22,9 @@
 namespace {
 
 constexpr int HEAD_THREADS = 256;
-constexpr int HEAD_R = 8;    // seed rows per CTA
+constexpr int HEAD_R = 4;    // seed rows per CTA (256 CTAs at B = 1024, two per SM)
 constexpr int HEAD_KC = 16;  // W1 rows per staged chunk
-constexpr int HEAD_S = 4;    // chunk buffers in the cp.async ring (HEAD_S - 1 chunks in flight)
+constexpr int HEAD_S = 3;    // chunk buffers in the cp.async ring (HEAD_S - 1 chunks in flight)
 
 __device__ __forceinline__ float warp_sum(float v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -64,20 +64,37 @@ __device__ __forceinline__ void stage_w1(float* ring, const float* W1, int H, in
 }
 
 template <int R>
+__device__ __forceinline__ void fma_rows(const float* col, float w, float (&acc)[R]) {
+#pragma unroll
+  for (int q = 0; q < R / 4; ++q) {
+    const float4 x = *reinterpret_cast<const float4*>(col + 4 * q);
+    acc[4 * q + 0] = fmaf(x.x, w, acc[4 * q + 0]);
+    acc[4 * q + 1] = fmaf(x.y, w, acc[4 * q + 1]);
+    acc[4 * q + 2] = fmaf(x.z, w, acc[4 * q + 2]);
+    acc[4 * q + 3] = fmaf(x.w, w, acc[4 * q + 3]);
+  }
+}
+
+// Row-indexed shared arrays are stored transposed ([k][R], [j][R], [c][R]) so one pair of 16-byte
+// broadcast loads feeds R = 8 FMAs.
+template <int R>
 __global__ void __launch_bounds__(HEAD_THREADS) k_head_rows(HeadArgs a) {
+  static_assert(R % 4 == 0, "float4 loads along the transposed columns");
   extern __shared__ __align__(16) float sm[];
   const int D = a.D, D2 = 2 * D, H = a.H, C = a.C;
-  float* ring = sm;                        // [HEAD_S][KC][H] W1 chunk ring
-  float* w2 = ring + HEAD_S * HEAD_KC * H;  // [H][C]
-  float* hh = w2 + ((H * C + 3) & ~3);  // [R][H]
-  float* dh = hh + R * H;            // [R][H]
-  float* dl = dh + R * H;            // [R][C]
-  float* cc = dl + R * C;            // [R][2D]
+  float* ring = sm;                              // [HEAD_S][KC][H] W1 chunk ring
+  float* w2 = ring + HEAD_S * HEAD_KC * H;       // [H][C]
+  float* ht = w2 + ((H * C + 3) & ~3);           // hidden^T [H][R]
+  float* dht = ht + H * R;                       // dhidden^T [H][R]
+  float* dl = dht + H * R;                       // logits [R][C]
+  float* dlt = dl + ((R * C + 3) & ~3);          // dlogits^T [C][R]
+  float* part = dlt + C * R;                     // logit partials [4][C][R]
+  float* cct = part + 4 * C * R;                 // concat^T [2D][R]
   const int r0 = blockIdx.x * R;
   const int nr = min(R, a.B - r0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
 
-  {  // W2 (whole) and the first W1 chunk in flight while the concat rows load
+  {  // W2 (whole) and the first W1 chunks in flight while the concat rows load
     const int q = (H * C) >> 2;
     for (int i = threadIdx.x; i < q; i += blockDim.x) cpa16(w2 + i * 4, a.W2 + i * 4);
     cpa_commit();
@@ -91,7 +108,7 @@ __global__ void __launch_bounds__(HEAD_THREADS) k_head_rows(HeadArgs a) {
       const int64_t row = r0 + r;
       v = k < D ? a.X[a.seeds[row] * a.xs + k] : a.agg[row * a.as + (k - D)];
     }
-    cc[i] = v;
+    cct[k * R + r] = v;
   }
 
   // hidden = ReLU(concat W1 + b1): thread j keeps R accumulators per column it owns
@@ -111,16 +128,15 @@ __global__ void __launch_bounds__(HEAD_THREADS) k_head_rows(HeadArgs a) {
     for (int u = 0; u < JMAX; ++u) {
       const int j = threadIdx.x + u * blockDim.x;
       if (j < H) {
+#pragma unroll 4
         for (int t = 0; t < n; ++t) {
-          const float wv = w[t * H + j];
-#pragma unroll
-          for (int r = 0; r < R; ++r) acc[u][r] = fmaf(cc[r * D2 + k0 + t], wv, acc[u][r]);
+          fma_rows<R>(cct + (k0 + t) * R, w[t * H + j], acc[u]);
         }
       }
     }
     __syncthreads();
   }
-  // the d_x_agg pass streams W1[D:] through the same buffers: start its first chunk now
+  // the d_x_agg pass streams W1[D:] through the same ring: start its first chunks now
   const int nch2 = (D + HEAD_KC - 1) / HEAD_KC;
   for (int c = 0; c < HEAD_S - 1; ++c) stage_w1(ring, a.W1, H, D, D, c);
 #pragma unroll
@@ -131,25 +147,39 @@ __global__ void __launch_bounds__(HEAD_THREADS) k_head_rows(HeadArgs a) {
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const float h = acc[u][r] + bj;
-        hh[r * H + j] = h > 0.f ? h : 0.f;
+        ht[j * R + r] = h > 0.f ? h : 0.f;
       }
     }
   }
   __syncthreads();
 
-  for (int i = threadIdx.x; i < R * C; i += blockDim.x) {  // logits = hidden W2 + b2
+  // logits = hidden W2 + b2: thread (g, c) sums j in [g*H/4, (g+1)*H/4) for all R rows; the four
+  // partials are added in g order
+  const int hq = (H + 3) >> 2;
+  for (int i = threadIdx.x; i < 4 * C; i += blockDim.x) {
+    const int g = i / C, c = i - g * C;
+    float s[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) s[r] = 0.f;
+    const int j1 = min(H, (g + 1) * hq);
+    for (int j = g * hq; j < j1; ++j) {
+      fma_rows<R>(ht + j * R, w2[j * C + c], s);
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) part[(g * C + c) * R + r] = s[r];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < R * C; i += blockDim.x) {
     const int r = i / C, c = i - r * C;
-    float s = 0.f;
-    const float* hr = hh + r * H;
-    for (int j = 0; j < H; ++j) s = fmaf(hr[j], w2[j * C + c], s);
-    dl[i] = s + a.b2[c];
+    const float v = ((part[c * R + r] + part[(C + c) * R + r]) + part[(2 * C + c) * R + r]) + part[(3 * C + c) * R + r];
+    dl[i] = v + a.b2[c];
   }
   __syncthreads();
 
   for (int r = warp; r < R; r += nw) {  // softmax cross-entropy, dlogits (train.py:123-139)
-    float* L = dl + r * C;
+    const float* L = dl + r * C;
     if (r >= nr) {  // padding rows: keep them finite and inert
-      for (int c = lane; c < C; c += 32) L[c] = 0.f;
+      for (int c = lane; c < C; c += 32) dlt[c * R + r] = 0.f;
       continue;
     }
     float m = -INFINITY;
@@ -162,11 +192,10 @@ __global__ void __launch_bounds__(HEAD_THREADS) k_head_rows(HeadArgs a) {
     const int64_t y = a.labels[r0 + r];
     const bool bad = y < 0 || y >= C;
     const float ly = bad ? NAN : (L[bad ? 0 : y] - m) - lse;
-    __syncwarp();
     const float fB = (float)a.B;
     for (int c = lane; c < C; c += 32) {
       const float p = expf(L[c] - m) / s;
-      L[c] = bad ? NAN : (p - (c == y ? 1.f : 0.f)) / fB;
+      dlt[c * R + r] = bad ? NAN : (p - (c == y ? 1.f : 0.f)) / fB;
     }
     if (lane == 0) a.lrow[r0 + r] = -ly;
   }
@@ -177,14 +206,12 @@ __global__ void __launch_bounds__(HEAD_THREADS) k_head_rows(HeadArgs a) {
 #pragma unroll
     for (int r = 0; r < R; ++r) s[r] = 0.f;
     for (int c = 0; c < C; ++c) {
-      const float w = w2[j * C + c];
-#pragma unroll
-      for (int r = 0; r < R; ++r) s[r] = fmaf(dl[r * C + c], w, s[r]);
+      fma_rows<R>(dlt + c * R, w2[j * C + c], s);
     }
 #pragma unroll
-    for (int r = 0; r < R; ++r) dh[r * H + j] = s[r] * (hh[r * H + j] > 0.f ? 1.f : 0.f);
+    for (int r = 0; r < R; ++r) dht[j * R + r] = s[r] * (ht[j * R + r] > 0.f ? 1.f : 0.f);
   }
-  // (the chunk loop's first barrier orders these dh writes before their reads)
+  // (the chunk loop's first barrier orders these dht writes before their reads)
 
   for (int c = 0; c < nch2; ++c) {  // d_x_agg[r][k] = sum_j dhidden[r][j] W1[D + k][j]
     const int k0 = c * HEAD_KC, n = min(HEAD_KC, D - k0);
@@ -197,9 +224,7 @@ __global__ void __launch_bounds__(HEAD_THREADS) k_head_rows(HeadArgs a) {
 #pragma unroll
       for (int r = 0; r < R; ++r) s[r] = 0.f;
       for (int j = lane; j < H; j += 32) {
-        const float wj = w[t * H + j];
-#pragma unroll
-        for (int r = 0; r < R; ++r) s[r] = fmaf(dh[r * H + j], wj, s[r]);
+        fma_rows<R>(dht + j * R, w[t * H + j], s);
       }
       float mine = 0.f;
 #pragma unroll
@@ -215,21 +240,28 @@ __global__ void __launch_bounds__(HEAD_THREADS) k_head_rows(HeadArgs a) {
   const int D21 = D2 + 1, H1 = H + 1;  // [concat | 1], [hidden | 1], dhidden, dlogits rows
   for (int i = threadIdx.x; i < nr * D21; i += blockDim.x) {
     const int r = i / D21, k = i - r * D21;
-    a.cat1[(int64_t)(r0 + r) * D21 + k] = k < D2 ? cc[r * D2 + k] : 1.f;
+    a.cat1[(int64_t)(r0 + r) * D21 + k] = k < D2 ? cct[k * R + r] : 1.f;
   }
   for (int i = threadIdx.x; i < nr * H1; i += blockDim.x) {
     const int r = i / H1, j = i - r * H1;
-    a.hid1[(int64_t)(r0 + r) * H1 + j] = j < H ? hh[r * H + j] : 1.f;
+    a.hid1[(int64_t)(r0 + r) * H1 + j] = j < H ? ht[j * R + r] : 1.f;
   }
-  for (int i = threadIdx.x; i < nr * H; i += blockDim.x) a.dhid[(int64_t)r0 * H + i] = dh[i];
-  for (int i = threadIdx.x; i < nr * C; i += blockDim.x) a.dlog[(int64_t)r0 * C + i] = dl[i];
+  for (int i = threadIdx.x; i < nr * H; i += blockDim.x) {
+    const int r = i / H, j = i - r * H;
+    a.dhid[(int64_t)r0 * H + i] = dht[j * R + r];
+  }
+  for (int i = threadIdx.x; i < nr * C; i += blockDim.x) {
+    const int r = i / C, c = i - r * C;
+    a.dlog[(int64_t)r0 * C + i] = dlt[c * R + r];
+  }
 }
 
 inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 size_t rows_smem(int D, int H, int C) {
-  return ((size_t)HEAD_S * HEAD_KC * H + (((size_t)H * C + 3) & ~(size_t)3) + (size_t)HEAD_R * (2 * H + C + 2 * D)) *
-         sizeof(float);
+  const size_t hc = ((size_t)H * C + 3) & ~(size_t)3, rc = ((size_t)HEAD_R * C + 3) & ~(size_t)3;
+  return ((size_t)HEAD_S * HEAD_KC * H + hc + (size_t)HEAD_R * 2 * H + rc + (size_t)C * HEAD_R * 5 +
+          (size_t)HEAD_R * 2 * D) * sizeof(float);
 }
 
 }  // namespace
