@@ -283,6 +283,18 @@ int fsa_umod(const uint64_t* x, const uint32_t* m, int64_t n, uint32_t* out, voi
  * [hidden | 1]^T dlogits = [dW2; db2] and loss = mean(row losses). Row-major, element strides;
  * H % 4 == 0, H <= 512, W1 / W2 16-byte aligned. Labels outside [0, C) give NaN rows. One
  * kernel on `stream`. */
+/* AdamW of the training step (fp32; pkg/src/fsa/train.py:163-184) over n_tensors (<= 8)
+ * parameter / gradient / first-moment / second-moment arrays of sizes[k] elements (host arrays of
+ * device pointers). When every gradient element is finite: *step_count (device double) += 1, the
+ * bias corrections are derived from it in double, and every parameter takes the reference's
+ * update in its operation order (fp32, no contraction); *ok_out (device byte) = 1. Otherwise
+ * nothing changes and *ok_out = 0 (the reference raises NonFiniteGradientError). A memset and
+ * two kernels on `stream`; ws: fsa_adamw_ws_bytes() bytes of device scratch. */
+size_t fsa_adamw_ws_bytes(void);
+int fsa_adamw_step(int n_tensors, float* const* params, const float* const* grads, float* const* exp_avg,
+                   float* const* exp_avg_sq, const int64_t* sizes, double* step_count, double lr, double beta1,
+                   double beta2, double weight_decay, double eps, unsigned char* ok_out, void* ws, size_t ws_bytes,
+                   void* stream);
 size_t fsa_sage_head_ws_bytes(int64_t B, int32_t D, int32_t H, int32_t C);
 size_t fsa_sage_head_smem_bytes(int32_t D, int32_t H, int32_t C);
 int fsa_sage_head_rows(const float* X, int64_t x_stride, const int64_t* seeds, const float* agg, int64_t agg_stride,

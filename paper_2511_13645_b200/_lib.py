@@ -58,6 +58,9 @@ SIGNATURES = {
     "fsa_fused_2hop_bwd_phase": (_int, [_p, _i64, _i64, _i64, _int, _p, _p, _i32, _i32, _i64, _p, _int, _p,
                                         _p, _p, _p, _sz, _p, _int]),
     "fsa_zero_rows": (_int, [_p, _i64, _int, _p, _i64, _p]),
+    "fsa_adamw_ws_bytes": (_sz, []),
+    "fsa_adamw_step": (_int, [_int, _p, _p, _p, _p, _p, _p, C.c_double, C.c_double, C.c_double, C.c_double,
+                              C.c_double, _p, _p, _sz, _p]),
     "fsa_sage_head_ws_bytes": (_sz, [_i64, _i32, _i32, _i32]),
     "fsa_sage_head_smem_bytes": (_sz, [_i32, _i32, _i32]),
     "fsa_sage_head_rows": (_int, [_p, _i64, _p, _p, _i64, _p, _i64, _i32, _i32, _i32, _p, _p, _p, _p, _p, _i64,

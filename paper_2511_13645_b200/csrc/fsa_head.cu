@@ -17,6 +17,8 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "../../include/fsa_b200.h"
 
 namespace {
@@ -307,5 +309,131 @@ extern "C" int fsa_sage_head_rows(const float* X, int64_t x_stride, const int64_
   if (e != cudaSuccess) return FSA_ERR_CUDA;
   k_head_rows<HEAD_R><<<(unsigned)((B + HEAD_R - 1) / HEAD_R), HEAD_THREADS, smem, st>>>(a);
   e = cudaGetLastError();
+  return e == cudaSuccess ? FSA_OK : FSA_ERR_CUDA;
+}
+
+// ---------------------------------------------------------------------------------------------
+// AdamW of the training step (reference: pkg/src/fsa/train.py:163-184), fp32 parameters, as two
+// grid-wide kernels instead of multi-tensor launches that give each 64 K-element chunk one CTA:
+//   k_adamw_check   every gradient element finite? (flag); the last CTA to finish advances the
+//                   device step count by `ok` and derives the bias corrections in double, as the
+//                   reference does (it raises before incrementing, so a skipped step does not count)
+//   k_adamw_update  p -= lr*wd*p; m = b1*m + (1-b1)*g; v = b2*v + (1-b2)*g*g;
+//                   p -= lr*(m/bc1)/(sqrt(v/bc2)+eps), each operation rounded in fp32 in the
+//                   reference's order (no contraction); nothing is written when a gradient is
+//                   non-finite.
+namespace {
+
+constexpr int ADAMW_MAX = 8;
+constexpr int ADAMW_THREADS = 256;
+
+struct AdamwArgs {
+  int n;
+  float* p[ADAMW_MAX];
+  const float* g[ADAMW_MAX];
+  float* m[ADAMW_MAX];
+  float* v[ADAMW_MAX];
+  int64_t off[ADAMW_MAX + 1];  // prefix sums of the tensor sizes
+  double* t;                   // device step count
+  unsigned char* ok;           // device bool
+  unsigned* flag;              // [0] non-finite seen, [1] CTAs done
+  float* coef;                 // [0] bc1, [1] bc2 (fp32, as the reference's weak scalars)
+  double beta1, beta2;
+  float lr_wd, one_m_b1, one_m_b2, b1f, b2f, lr, eps;
+};
+
+__device__ __forceinline__ int adamw_tensor(const AdamwArgs& a, int64_t i) {
+  int k = 0;
+  while (k + 1 < a.n && i >= a.off[k + 1]) ++k;
+  return k;
+}
+
+__global__ void __launch_bounds__(ADAMW_THREADS) k_adamw_check(AdamwArgs a) {
+  const int64_t total = a.off[a.n];
+  bool bad = false;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int k = adamw_tensor(a, i);
+    bad |= !isfinite(a.g[k][i - a.off[k]]);
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&a.flag[0], 1u);
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&a.flag[1], 1u) == gridDim.x - 1) {  // last CTA: every flag update is visible
+      __threadfence();
+      const bool ok = atomicAdd(&a.flag[0], 0u) == 0u;
+      const double t = *a.t + (ok ? 1.0 : 0.0);
+      *a.t = t;
+      *a.ok = ok ? 1 : 0;
+      a.coef[0] = (float)(1.0 - pow(a.beta1, t));
+      a.coef[1] = (float)(1.0 - pow(a.beta2, t));
+    }
+  }
+}
+
+__global__ void __launch_bounds__(ADAMW_THREADS) k_adamw_update(AdamwArgs a) {
+  if (!*a.ok) return;
+  const float bc1 = a.coef[0], bc2 = a.coef[1];
+  const int64_t total = a.off[a.n];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int k = adamw_tensor(a, i);
+    const int64_t e = i - a.off[k];
+    const float g = a.g[k][e];
+    float p = a.p[k][e];
+    p = __fsub_rn(p, __fmul_rn(a.lr_wd, p));
+    const float m = __fadd_rn(__fmul_rn(a.m[k][e], a.b1f), __fmul_rn(a.one_m_b1, g));
+    const float v = __fadd_rn(__fmul_rn(a.v[k][e], a.b2f), __fmul_rn(a.one_m_b2, __fmul_rn(g, g)));
+    const float den = __fadd_rn(__fsqrt_rn(__fdiv_rn(v, bc2)), a.eps);
+    p = __fsub_rn(p, __fdiv_rn(__fmul_rn(a.lr, __fdiv_rn(m, bc1)), den));
+    a.m[k][e] = m;
+    a.v[k][e] = v;
+    a.p[k][e] = p;
+  }
+}
+
+}  // namespace
+
+extern "C" size_t fsa_adamw_ws_bytes(void) { return 16; }
+
+extern "C" int fsa_adamw_step(int n_tensors, float* const* params, const float* const* grads, float* const* exp_avg,
+                              float* const* exp_avg_sq, const int64_t* sizes, double* step_count, double lr,
+                              double beta1, double beta2, double weight_decay, double eps, unsigned char* ok_out,
+                              void* ws, size_t ws_bytes, void* stream) {
+  if (n_tensors <= 0 || n_tensors > ADAMW_MAX || !params || !grads || !exp_avg || !exp_avg_sq || !sizes ||
+      !step_count || !ok_out || !ws)
+    return FSA_ERR_ARG;
+  if (ws_bytes < fsa_adamw_ws_bytes()) return FSA_ERR_WORKSPACE;
+  AdamwArgs a{};
+  a.n = n_tensors;
+  a.off[0] = 0;
+  for (int k = 0; k < n_tensors; ++k) {
+    if (!params[k] || !grads[k] || !exp_avg[k] || !exp_avg_sq[k] || sizes[k] < 0) return FSA_ERR_ARG;
+    a.p[k] = params[k];
+    a.g[k] = grads[k];
+    a.m[k] = exp_avg[k];
+    a.v[k] = exp_avg_sq[k];
+    a.off[k + 1] = a.off[k] + sizes[k];
+  }
+  a.t = step_count;
+  a.ok = ok_out;
+  a.flag = static_cast<unsigned*>(ws);
+  a.coef = reinterpret_cast<float*>(static_cast<char*>(ws) + 8);
+  a.beta1 = beta1;
+  a.beta2 = beta2;
+  // the reference's scalars: python floats meeting float32 arrays (numpy weak scalars -> fp32)
+  a.lr_wd = (float)(lr * weight_decay);
+  a.one_m_b1 = (float)(1.0 - beta1);
+  a.one_m_b2 = (float)(1.0 - beta2);
+  a.b1f = (float)beta1;
+  a.b2f = (float)beta2;
+  a.lr = (float)lr;
+  a.eps = (float)eps;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (cudaMemsetAsync(ws, 0, 8, st) != cudaSuccess) return FSA_ERR_CUDA;
+  const int64_t total = a.off[n_tensors];
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(296, (total + ADAMW_THREADS * 4 - 1) /
+                                                                                   (ADAMW_THREADS * 4)));
+  k_adamw_check<<<grid, ADAMW_THREADS, 0, st>>>(a);
+  k_adamw_update<<<grid, ADAMW_THREADS, 0, st>>>(a);
+  const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? FSA_OK : FSA_ERR_CUDA;
 }

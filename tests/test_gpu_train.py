@@ -221,3 +221,32 @@ def test_sage_head_bad_label_gives_nonfinite_update_skip():
     assert not bool(train.adamw_step(state, grads))
     for k in train.PARAM_NAMES:
         assert torch.equal(getattr(state, k), before[k])
+
+
+def test_adamw_kernel_matches_reference_update():
+    """fsa_adamw_step (train.adamw_step on fp32 CUDA state) against the reference's numpy update
+    (train.py:163-184) over three steps: same operation order in fp32, so bitwise."""
+    from paper_2511_13645_b200 import train
+    state = train.init_train_state(12, 16, 5, base_seed=4)
+    rng = np.random.default_rng(9)
+    P = {k: getattr(state, k).cpu().numpy().copy() for k in train.PARAM_NAMES}
+    M = {k: np.zeros_like(v) for k, v in P.items()}
+    V = {k: np.zeros_like(v) for k, v in P.items()}
+    h = state.hyper
+    for t in range(1, 4):
+        G = {k: rng.standard_normal(v.shape).astype(np.float32) for k, v in P.items()}
+        assert bool(train.adamw_step(state, {k: torch.from_numpy(g).cuda() for k, g in G.items()}))
+        bc1, bc2 = 1.0 - h.beta1 ** t, 1.0 - h.beta2 ** t
+        for k in P:
+            p, m, v, g = P[k], M[k], V[k], G[k]
+            p -= h.lr * h.weight_decay * p
+            m *= h.beta1
+            m += (1.0 - h.beta1) * g
+            v *= h.beta2
+            v += (1.0 - h.beta2) * (g * g)
+            p -= h.lr * (m / bc1) / (np.sqrt(v / bc2) + h.eps)
+    assert state.step_count == 3
+    for k in P:
+        np.testing.assert_array_equal(getattr(state, k).cpu().numpy(), P[k])
+        np.testing.assert_array_equal(state.m[k].cpu().numpy(), M[k])
+        np.testing.assert_array_equal(state.v[k].cpu().numpy(), V[k])
