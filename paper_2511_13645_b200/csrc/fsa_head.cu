@@ -28,6 +28,22 @@ constexpr int HEAD_R = 4;    // seed rows per CTA (256 CTAs at B = 1024, two per
 constexpr int HEAD_KC = 16;  // W1 rows per staged chunk
 constexpr int HEAD_S = 3;    // chunk buffers in the cp.async ring (HEAD_S - 1 chunks in flight)
 
+#ifdef HEAD_TRACE  // per-CTA phase timestamps (instrumented builds only: -DHEAD_TRACE, tools/head_trace.py)
+__device__ unsigned long long g_head_trace[1024][9];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define HEAD_TRACE_START() \
+  if (threadIdx.x == 0 && blockIdx.x < 1024) g_head_trace[blockIdx.x][0] = gtimer()
+#define HEAD_MARK(i) \
+  if (threadIdx.x == 0 && blockIdx.x < 1024) g_head_trace[blockIdx.x][(i) + 1] = gtimer()
+#else
+#define HEAD_TRACE_START()
+#define HEAD_MARK(i)
+#endif
+
 __device__ __forceinline__ float warp_sum(float v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
@@ -95,6 +111,7 @@ __global__ void __launch_bounds__(HEAD_THREADS) k_head_rows(HeadArgs a) {
   const int r0 = blockIdx.x * R;
   const int nr = min(R, a.B - r0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  HEAD_TRACE_START();
 
   {  // W2 (whole) and the first W1 chunks in flight while the concat rows load
     const int q = (H * C) >> 2;
@@ -113,6 +130,7 @@ __global__ void __launch_bounds__(HEAD_THREADS) k_head_rows(HeadArgs a) {
     cct[k * R + r] = v;
   }
 
+  HEAD_MARK(0);
   // hidden = ReLU(concat W1 + b1): thread j keeps R accumulators per column it owns
   constexpr int JMAX = 2;  // H <= JMAX * blockDim.x
   float acc[JMAX][R];
@@ -138,6 +156,7 @@ __global__ void __launch_bounds__(HEAD_THREADS) k_head_rows(HeadArgs a) {
     }
     __syncthreads();
   }
+  HEAD_MARK(1);
   // the d_x_agg pass streams W1[D:] through the same ring: start its first chunks now
   const int nch2 = (D + HEAD_KC - 1) / HEAD_KC;
   for (int c = 0; c < HEAD_S - 1; ++c) stage_w1(ring, a.W1, H, D, D, c);
@@ -155,6 +174,7 @@ __global__ void __launch_bounds__(HEAD_THREADS) k_head_rows(HeadArgs a) {
   }
   __syncthreads();
 
+  HEAD_MARK(2);
   // logits = hidden W2 + b2: thread (g, c) sums j in [g*H/4, (g+1)*H/4) for all R rows; the four
   // partials are added in g order
   const int hq = (H + 3) >> 2;
@@ -178,6 +198,7 @@ __global__ void __launch_bounds__(HEAD_THREADS) k_head_rows(HeadArgs a) {
   }
   __syncthreads();
 
+  HEAD_MARK(3);
   for (int r = warp; r < R; r += nw) {  // softmax cross-entropy, dlogits (train.py:123-139)
     const float* L = dl + r * C;
     if (r >= nr) {  // padding rows: keep them finite and inert
@@ -203,6 +224,7 @@ __global__ void __launch_bounds__(HEAD_THREADS) k_head_rows(HeadArgs a) {
   }
   __syncthreads();
 
+  HEAD_MARK(4);
   for (int j = threadIdx.x; j < H; j += blockDim.x) {  // dhidden = (dlogits W2^T) * (hidden > 0)
     float s[R];
 #pragma unroll
@@ -215,6 +237,7 @@ __global__ void __launch_bounds__(HEAD_THREADS) k_head_rows(HeadArgs a) {
   }
   // (the chunk loop's first barrier orders these dht writes before their reads)
 
+  HEAD_MARK(5);
   for (int c = 0; c < nch2; ++c) {  // d_x_agg[r][k] = sum_j dhidden[r][j] W1[D + k][j]
     const int k0 = c * HEAD_KC, n = min(HEAD_KC, D - k0);
     stage_w1(ring, a.W1, H, D, D, c + HEAD_S - 1);
@@ -239,6 +262,7 @@ __global__ void __launch_bounds__(HEAD_THREADS) k_head_rows(HeadArgs a) {
     __syncthreads();
   }
 
+  HEAD_MARK(6);
   const int D21 = D2 + 1, H1 = H + 1;  // [concat | 1], [hidden | 1], dhidden, dlogits rows
   for (int i = threadIdx.x; i < nr * D21; i += blockDim.x) {
     const int r = i / D21, k = i - r * D21;
@@ -256,6 +280,7 @@ __global__ void __launch_bounds__(HEAD_THREADS) k_head_rows(HeadArgs a) {
     const int r = i / C, c = i - r * C;
     a.dlog[(int64_t)r0 * C + i] = dlt[c * R + r];
   }
+  HEAD_MARK(7);
 }
 
 inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -437,3 +462,9 @@ extern "C" int fsa_adamw_step(int n_tensors, float* const* params, const float* 
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? FSA_OK : FSA_ERR_CUDA;
 }
+
+#ifdef HEAD_TRACE
+extern "C" int fsa_head_trace_read(unsigned long long* host, int nblocks) {
+  return cudaMemcpyFromSymbol(host, g_head_trace, sizeof(unsigned long long) * 9 * (size_t)nblocks) == cudaSuccess ? 0 : 4;
+}
+#endif
