@@ -288,8 +288,9 @@ int fsa_umod(const uint64_t* x, const uint32_t* m, int64_t n, uint32_t* out, voi
  * device pointers). When every gradient element is finite: *step_count (device double) += 1, the
  * bias corrections are derived from it in double, and every parameter takes the reference's
  * update in its operation order (fp32, no contraction); *ok_out (device byte) = 1. Otherwise
- * nothing changes and *ok_out = 0 (the reference raises NonFiniteGradientError). A memset and
- * two kernels on `stream`; ws: fsa_adamw_ws_bytes() bytes of device scratch. */
+ * nothing changes and *ok_out = 0 (the reference raises NonFiniteGradientError). Two kernels on
+ * `stream`; ws: fsa_adamw_ws_bytes() bytes of device scratch, zero before the first call (the
+ * kernels leave it zero, so a persistent buffer needs no memset per step). */
 size_t fsa_adamw_ws_bytes(void);
 int fsa_adamw_step(int n_tensors, float* const* params, const float* const* grads, float* const* exp_avg,
                    float* const* exp_avg_sq, const int64_t* sizes, double* step_count, double lr, double beta1,

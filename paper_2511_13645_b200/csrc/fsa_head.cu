@@ -386,6 +386,8 @@ __global__ void __launch_bounds__(ADAMW_THREADS) k_adamw_check(AdamwArgs a) {
     if (atomicAdd(&a.flag[1], 1u) == gridDim.x - 1) {  // last CTA: every flag update is visible
       __threadfence();
       const bool ok = atomicAdd(&a.flag[0], 0u) == 0u;
+      a.flag[0] = 0u;  // leave the scratch zero for the next call
+      a.flag[1] = 0u;
       const double t = *a.t + (ok ? 1.0 : 0.0);
       *a.t = t;
       *a.ok = ok ? 1 : 0;
@@ -453,7 +455,6 @@ extern "C" int fsa_adamw_step(int n_tensors, float* const* params, const float* 
   a.lr = (float)lr;
   a.eps = (float)eps;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (cudaMemsetAsync(ws, 0, 8, st) != cudaSuccess) return FSA_ERR_CUDA;
   const int64_t total = a.off[n_tensors];
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(296, (total + ADAMW_THREADS * 4 - 1) /
                                                                                    (ADAMW_THREADS * 4)));
