@@ -456,8 +456,9 @@ extern "C" int fsa_adamw_step(int n_tensors, float* const* params, const float* 
   a.eps = (float)eps;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int64_t total = a.off[n_tensors];
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(296, (total + ADAMW_THREADS * 4 - 1) /
-                                                                                   (ADAMW_THREADS * 4)));
+  // one element per thread up to 8 CTAs per SM of a 148-SM part: the loops are latency-bound
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(148 * 8, (total + ADAMW_THREADS - 1) /
+                                                                                      ADAMW_THREADS));
   k_adamw_check<<<grid, ADAMW_THREADS, 0, st>>>(a);
   k_adamw_update<<<grid, ADAMW_THREADS, 0, st>>>(a);
   const cudaError_t e = cudaGetLastError();
